@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""Benchmark of the fused RK4 finite-difference step (BASELINE.json metric:
+"grid-point updates/s per RK4 step (fp64) at 1/2/4/8 B200; % HBM roofline").
+
+Default workload (N=1): configs[1], the scalar wave equation Eq. 1,
+4th-order FD, 512^3 fp64, periodic, 3 ghosts, fused RHS + RK4 update.  A step is one
+classical RK4 step of the whole grid = the 4 fused stage kernels.  Inputs (23 GB of state)
+are larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): z-slab decomposition, 512^3 per GPU (weak
+scaling; global grid 512 x 512 x 512N), halo exchange fused into the stage kernels over
+CUDA-IPC peer memory with stream-memop flags.
+
+``--impl reference``: the CPU oracle (oracle/), timed as it stands on this host's cores on a
+bounded sample of the same workload (there is no reference implementation of the paper).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+BYTES_PER_POINT = {"wave": 432, "bssn": 2400}   # DESIGN.md §Roofline (one HBM pass per stage)
+METRIC = "grid-point updates/s per RK4 step (fp64)"
+
+
+def measured_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0, period_ms=200):
+        self.index, self.period = index, period_ms
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", str(self.period)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_cores():
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n else os.cpu_count()
+
+
+def oracle_sample(system: str, seconds_target: float = 15.0):
+    """Time the CPU oracle as it stands on a bounded sample of the workload: the same
+    per-point RK4 step on a smaller periodic grid, repeated until ~seconds_target."""
+    import chemora_inputs as ci
+    import oracle
+    if system == "wave":
+        n = 160
+        h = (2 * math.pi / n,) * 3
+        y = ci.noise((n, n, n), 5, seed=1410)
+        sysid = oracle.WAVE
+        params = None
+    else:
+        n = 48
+        h = (1.0 / n,) * 3
+        y = ci.mink_pert((n, n, n), h, seed=1410)
+        sysid = oracle.BSSN
+        params = oracle.default_bssn_params()
+    dt = 0.25 * h[0]
+    steps, elapsed = 0, 0.0
+    while elapsed < seconds_target:
+        t0 = time.perf_counter()
+        y = oracle.rk4(sysid, y, h, dt, 1, params)
+        elapsed += time.perf_counter() - t0
+        steps += 1
+    return {"value": n ** 3 * steps / elapsed, "unit": "grid-point updates/s", "cores": cpu_cores(),
+            "kind": "oracle", "sample": f"{system} {n}^3 periodic, {steps} RK4 steps, "
+            f"{elapsed:.1f} s, OMP over z"}, n, steps, elapsed
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    cfg = workload(args)
+    per = max(2.0, 20.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(cfg["system"], per / 4)
+    cb, n, steps, elapsed = oracle_sample(cfg["system"], per * args.steps)
+    line = {"metric": METRIC, "value": cb["value"], "unit": "grid-point updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference", "config": cfg["config"],
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "grid-point updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload(args):
+    if args.config == "wave512":
+        n = (512, 512, 512)
+        return {"system": "wave", "n": n,
+                "config": {"workload": "scalar wave eq (Eq. 1), 4th-order FD, 512^3 fp64 per GPU, "
+                           "periodic, 3 ghost zones, fused RHS+RK4 (configs[1])",
+                           "grid": list(n), "ghost": 3, "fd_order": 4, "init": "PW3 plane waves",
+                           "l2": "state (23 GB) larger than L2; no flush needed"}}
+    if args.config == "bssn192":
+        n = (192, 192, 192)
+        return {"system": "bssn", "n": n,
+                "config": {"workload": "BSSN-like 25-GF Einstein RHS with upwinded advection, "
+                           "192^3 fp64 per GPU, periodic, 3 ghost zones, fused RHS+RK4 (configs[2])",
+                           "grid": list(n), "ghost": 3, "fd_order": 4, "init": "MINK_PERT eps=1e-3",
+                           "l2": "state (6.2 GB) larger than L2; no flush needed"}}
+    raise SystemExit(f"unknown config {args.config}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="chemora", choices=["chemora", "reference"])
+    ap.add_argument("--config", default="wave512", choices=["wave512", "bssn192"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1410_1764_b200 as P
+    from paper_1410_1764_b200 import capi as C
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload(args)
+    n = cfg["n"]
+    system = C.SYS_WAVE if cfg["system"] == "wave" else C.SYS_BSSN
+    gext = (n[0], n[1], n[2] * world)
+    L = 2 * math.pi if system == C.SYS_WAVE else 1.0
+    h = (L / n[0], L / n[1], L / n[2])
+    dt = 0.25 * min(h)
+    g = P.Grid(system, gext, h, device=local, rank=rank, nranks=world)
+    if world > 1:
+        g.connect_ipc()
+    init = C.INIT_PLANE_WAVES if system == C.SYS_WAVE else C.INIT_MINK_PERT
+    g.set_initial(init, seed=1410)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        g.rk4_step(dt, 1)
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        barrier()
+        ev[0].record(stream)
+        for s in range(args.steps):
+            g.rk4_step(dt, 1)
+            ev[s + 1].record(stream)
+        barrier()
+    step_ms = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    pts_local = n[0] * n[1] * n[2]
+    value = pts_local * world * args.steps / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel: the 4 fused stage kernels of one RK4 step
+    peak, peak_kind = measured_peaks()
+    mean_step_s = float(np.mean(step_ms)) * 1e-3
+    bpp = BYTES_PER_POINT[cfg["system"]]
+    achieved = bpp * pts_local / mean_step_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                "kernel": "fused RK4 stage kernels (4 launches = 1 step)",
+                "algorithmic_bytes_per_point": bpp,
+                "frac_of_nominal_8TBps": achieved / 8000.0}
+
+    # e2e through the public API with host buffers: per step, upload the state from pinned
+    # host memory, one RK4 step, download the state.
+    e2e = None
+    if args.e2e_steps > 0:
+        shape = g.interior_shape()
+        host_in = torch.empty(shape, dtype=torch.float64).pin_memory()
+        host_out = torch.empty(shape, dtype=torch.float64).pin_memory()
+        g.get_state(out=host_in.numpy())
+        hin, hout = host_in.numpy(), host_out.numpy()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            g.set_initial(C.INIT_HOST, hin)
+            g.rk4_step(dt, 1)
+            g.get_state(out=hout)
+        e1.record(stream)
+        barrier()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        nbytes = int(np.prod(shape)) * 8
+        e2e = {"value": pts_local * world * args.e2e_steps / (e_ms * 1e-3), "unit": "grid-point updates/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "what": "chemora_set_initial(HOST, pinned) + chemora_rk4_step(1) + chemora_get_state per step"}
+
+    if rank == 0:
+        cb = None
+        if world == 1 and not args.no_cpu_baseline:
+            cb = oracle_sample(cfg["system"], 15.0)[0]
+        cfgout = dict(cfg["config"])
+        cfgout["parallelism"] = f"z-slab x{world}" if world > 1 else "single GPU"
+        cfgout["global_grid"] = list(gext)
+        line = {"metric": METRIC, "value": value, "unit": "grid-point updates/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": cfgout, "roofline": roofline, "cpu_baseline": cb,
+                "e2e": e2e, "gpu_launches": 4 * args.steps, "clocks": clk.summary(),
+                "step_ms": step_ms}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -63,6 +63,20 @@ def coords(n, spacing, origin=(0.0, 0.0, 0.0)):
     return z[:, None, None], y[None, :, None], x[None, None, :]
 
 
+def noise_box(gext, n_gf, seed, lo, size):
+    """NOISE values on the box [lo, lo+size) of a periodic global grid of extents ``gext``
+    (indices wrap), so a sample of a huge grid can be regenerated on the host."""
+    nx, ny, nz = gext
+    i = (np.arange(lo[0], lo[0] + size[0]) % nx).astype(np.uint64)[None, None, :]
+    j = (np.arange(lo[1], lo[1] + size[1]) % ny).astype(np.uint64)[None, :, None]
+    k = (np.arange(lo[2], lo[2] + size[2]) % nz).astype(np.uint64)[:, None, None]
+    index = i + np.uint64(nx) * (j + np.uint64(ny) * k)
+    out = np.empty((n_gf, size[2], size[1], size[0]))
+    for g in range(n_gf):
+        out[g] = hash_uniform(seed, g, index)
+    return out
+
+
 def noise(n, n_gf, seed, z0=0, nz_global=None):
     """Uniform [-1,1) noise on every GF keyed by the GLOBAL index.
 

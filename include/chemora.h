@@ -1,0 +1,195 @@
+/* chemora.h -- C ABI of the B200-native fused RK4 finite-difference stencil library.
+ *
+ * The hot path of Chemora's method (arXiv:1410.1764, /root/reference/PAPER.md): a
+ * generated finite-difference loop kernel that evaluates the right-hand side of a system
+ * of PDE grid functions on a 3-D Cartesian grid with ghost zones (PAPER.md:320-347,
+ * Eq. 1 and the Sec. 3 loop listing), stepped in time by a Runge-Kutta method
+ * (PAPER.md:209-219), with the grid decomposed across devices by the driver
+ * (PAPER.md:200-207).  Every call below names the passage that defines its operation.
+ *
+ * Conventions
+ *  - fp64 everywhere.  Grid functions ("GF") are stored structure-of-arrays,
+ *    [gf][z][y][x] with x contiguous.  Host arrays passed in or out are INTERIOR-only,
+ *    [gf][Nz_local][Ny][Nx] (or padded [gf][Nz_local+2g][Ny+2g][Nx+2g] where stated).
+ *  - Device memory is OWNED BY THE CALLER: chemora_grid_required_bytes() says how much,
+ *    the caller allocates it (e.g. torch.empty(bytes, dtype=uint8, device=cuda)) and passes
+ *    it to chemora_grid_create(); it must outlive the handle and be 256-byte aligned.
+ *  - Streams are borrowed (cudaStream_t passed as void*; NULL = legacy default stream).
+ *    Calls ENQUEUE work on the stream and return; device faults and non-finite values
+ *    surface at the next synchronising call (chemora_get_state*, chemora_norms*).
+ *  - Every function returns a chemora_status; on failure a thread-local message is
+ *    available from chemora_last_error().  No function aborts the process.
+ *  - Boundary: periodic on all axes (reading R9).  With nranks > 1
+ *    the global grid is split into z-slabs of extent[2]/nranks planes (rank r owns global
+ *    planes [r*Nz/P, (r+1)*Nz/P)); x and y stay whole on every rank.
+ */
+#ifndef CHEMORA_H
+#define CHEMORA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chemora_grid_s* chemora_grid_t; /* opaque handle */
+
+enum chemora_status {
+  CHEMORA_OK = 0,
+  CHEMORA_E_INVALID = 1,     /* bad argument (NULL pointer, wrong n_gf, unknown kind ...) */
+  CHEMORA_E_SHAPE = 2,       /* extents / ghost width violate the grid invariants          */
+  CHEMORA_E_NOMEM = 3,       /* workspace too small or misaligned                          */
+  CHEMORA_E_CUDA = 4,        /* CUDA runtime/driver error (message has the CUDA string)    */
+  CHEMORA_E_PEER = 5,        /* multi-rank connectivity error                              */
+  CHEMORA_E_NONFINITE = 6,   /* NaN/Inf produced by a step (message names GF and step)     */
+  CHEMORA_E_UNSUPPORTED = 7  /* valid request this build does not implement                */
+};
+
+/* PDE systems.  WAVE: the first-order scalar wave equation, Eq. 1 (PAPER.md:320-327,
+ * Fig. 1), 5 GFs in order u, rho, v1, v2, v3.
+ * BSSN: the 25-GF BSSN-like Einstein system of SURVEY.md App. A (PAPER.md:686-688 says only
+ * "the Einstein equations ... several thousand floating point operations"; R7),
+ * GFs in the order phi, gt11 gt12 gt13 gt22 gt23 gt33, trK, At11..At33, Xt1..3, alpha, A,
+ * beta1..3, B1..3. */
+enum chemora_system { CHEMORA_SYS_WAVE = 1, CHEMORA_SYS_BSSN = 2 };
+
+/* Initial-data kinds for chemora_set_initial (Fig. 1 "Init"). */
+enum chemora_init {
+  CHEMORA_INIT_HOST = 0,        /* host_src: interior [gf][Nz_local][Ny][Nx]; ghosts filled  */
+  CHEMORA_INIT_HOST_PADDED = 1, /* host_src: padded [gf][Nz_local+2g][Ny+2g][Nx+2g]; ghosts
+                                   taken AS GIVEN (no fill) -- for polynomial tests          */
+  CHEMORA_INIT_PLANE_WAVES = 2, /* wave: the PW3 superposition of DESIGN.md §Inputs           */
+  CHEMORA_INIT_GAUSSIAN = 3,    /* wave: rho = A exp(-(r/W)^2/2) at the domain centre;
+                                   kind_params = {A, W} or NULL for {1, 0.5}                 */
+  CHEMORA_INIT_NOISE = 4,       /* every GF = SplitMix64(seed ^ (gf<<40 + I)) -> [-1,1),
+                                   I = global interior index i + Nx (j + Ny k)               */
+  CHEMORA_INIT_MINK_PERT = 5    /* BSSN: flat + seeded sines, kind_params = {eps} or NULL   */
+};
+
+/* Grid descriptor (SPEC.md:415-418 UniformGrid). */
+typedef struct {
+  int32_t system;       /* enum chemora_system                                          */
+  int32_t ghost;        /* ghost width g; must be >= the stencil radius (2 wave, 3 BSSN)  */
+  int32_t n_gf;         /* number of grid functions; must be 5 (WAVE) or 25 (BSSN)       */
+  int32_t device;       /* CUDA device ordinal the workspace lives on                    */
+  int64_t extent[3];    /* GLOBAL interior extents Nx, Ny, Nz; each >= 2g; Nz % nranks == 0,
+                           and Nz/nranks >= 2g                                           */
+  double origin[3];     /* x_i = origin + i * h                            */
+  double spacing[3];    /* h per axis                                                     */
+  int32_t rank;         /* z-slab index of this handle, 0 <= rank < nranks               */
+  int32_t nranks;       /* number of z-slabs (processes or local slabs)                  */
+  int32_t fd_order;     /* accuracy order of the centered stencils: 0 or 4 (default), or
+                           2, 6, 8 for WAVE ("arbitrary order ... run-time
+                           option"); requires ghost >= fd_order/2                         */
+  int32_t n_params;     /* number of entries in params                                   */
+  const double* params; /* BSSN gauge parameters F_alpha, n_alpha, L, eta_alpha,
+                           c_alpha_adv, C_beta, p_beta, S_B, eta, c_beta_adv (App. A.3);
+                           NULL = the benchmark gauge {2,1,1,0,1,0.75,0,1,1,1}. Copied. */
+} chemora_grid_desc;
+
+/* Library version string (static storage). */
+const char* chemora_version(void);
+
+/* Thread-local text describing the last non-OK return on this thread. */
+const char* chemora_last_error(void);
+
+/* Bytes of device workspace the grid needs (4 state sets of n_gf padded arrays: the
+ * y/Q/B/C scheme of DESIGN.md §RK4, plus reduction scratch and flags).  Validates desc. */
+int chemora_grid_required_bytes(const chemora_grid_desc* desc, size_t* bytes);
+
+/* Create a grid handle over a caller-owned device workspace of >= required bytes.
+ * Does not initialise the state (call chemora_set_initial). */
+int chemora_grid_create(const chemora_grid_desc* desc, void* dev_workspace, size_t bytes,
+                        chemora_grid_t* out);
+
+/* Destroy the handle (does not free the caller's workspace).  NULL is a no-op. */
+int chemora_grid_destroy(chemora_grid_t grid);
+
+/* Local geometry: local interior extents and the global z index of local plane 0. */
+int chemora_grid_local(chemora_grid_t grid, int64_t* local_extent3, int64_t* z0);
+
+/* Set the state vector y (Fig. 1 "Init").  kind = enum chemora_init.
+ * HOST / HOST_PADDED copy from host_src (pageable or pinned; the call waits for the copy
+ * to be read), the analytic kinds are generated on the device from GLOBAL coordinates.
+ * Every kind except HOST_PADDED ends with chemora_halo_exchange (collective when
+ * nranks > 1).  Resets the step counter and the non-finite flag. */
+int chemora_set_initial(chemora_grid_t grid, int kind, const double* host_src,
+                        const double* kind_params, uint64_t seed, void* stream);
+
+/* Copy the local interior of y to host_dst [gf][Nz_local][Ny][Nx]; synchronises the stream.
+ * Returns CHEMORA_E_NONFINITE if a previous step produced NaN/Inf (data still copied). */
+int chemora_get_state(chemora_grid_t grid, double* host_dst, void* stream);
+
+/* As chemora_get_state but padded [gf][Nz_local+2g][Ny+2g][Nx+2g], ghosts included. */
+int chemora_get_state_padded(chemora_grid_t grid, double* host_dst, void* stream);
+
+/* k = F(y) at every local interior point, ghosts of y used as they are (SPEC.md:442-450
+ * apply_kernel; the RHS of Eq. 1 or App. A).  dev_dst: device, n_gf x local interior,
+ * [gf][z][y][x], caller-owned. */
+int chemora_rhs(chemora_grid_t grid, double* dev_dst, void* stream);
+
+/* Advance y by nsteps classical RK4 steps of size dt.
+ * Each step is 4 fused stage kernels; each stage evaluates the RHS of its input, applies
+ * the RK4 update, writes the periodic ghost images of its output, and (nranks > 1) stores
+ * its boundary planes into the neighbours' ghost planes (the halo exchange, PAPER.md:
+ * 201-204, 346).  On return (stream-ordered) y's ghosts are consistent.  nranks > 1 with
+ * peers connected through chemora_grid_connect_ipc is collective over all ranks. */
+int chemora_rk4_step(chemora_grid_t grid, double dt, int32_t nsteps, void* stream);
+
+/* Same, for n local slabs of ONE global grid living in this process (all on one device,
+ * connected with chemora_grid_connect_local); stages are interleaved slab by slab on
+ * the one stream.  This is the single-device emulation of the multi-GPU path. */
+int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t nsteps,
+                           void* stream);
+
+/* Periodic ghost fill of y: x and y locally, z by wrap (nranks == 1) or by storing the
+ * boundary planes into the neighbours' ghost planes (nranks > 1) (
+ * SPEC.md:433-441 sync_ghosts).  Collective when nranks > 1. */
+int chemora_halo_exchange(chemora_grid_t grid, void* stream);
+int chemora_halo_exchange_multi(chemora_grid_t* grids, int32_t n, void* stream);
+
+/* Local reduction partials of y over the local interior (SPEC.md:469-477 reduce; Fig. 1
+ * "Energy"): out[3v+0] = sum f^2, out[3v+1] = max|f|, out[3v+2] = sum f
+ * for v < n_gf, then (WAVE) out[3 n_gf] = sum 1/2 (rho^2 + v.v).  Deterministic order.
+ * Synchronises the stream.  Returns CHEMORA_E_NONFINITE as chemora_get_state. */
+int chemora_norms_partial(chemora_grid_t grid, double* host_out, void* stream);
+
+/* Combine per-rank partials (rank-major, nranks x chemora_norms_len doubles) in rank order
+ * into L2 = sqrt(h^3 sum f^2), Linf, h^3 sum f (and the energy h^3 sum eps). */
+int chemora_norms_combine(const chemora_grid_desc* desc, const double* partials,
+                          int32_t nranks, double* out);
+
+/* Number of doubles chemora_norms / chemora_norms_partial write: 3 n_gf (+1 for WAVE). */
+int chemora_norms_len(int32_t system, int32_t n_gf);
+
+/* nranks == 1 convenience: partial + combine. */
+int chemora_norms(chemora_grid_t grid, double* host_out, void* stream);
+
+/* ---- multi-slab connectivity (z-slab ring, rank r's neighbours are r-1 and r+1 mod P) */
+
+/* Same-process slabs (emulation on one device): grids[r] has rank r of n. */
+int chemora_grid_connect_local(chemora_grid_t* grids, int32_t n);
+
+/* Cross-process: size of the opaque per-rank peer record, export this rank's record
+ * (cudaIpc handle of the workspace), and connect to the lower and upper neighbours'
+ * records (exchanged by the caller, e.g. torch.distributed.all_gather_object). */
+int chemora_peer_record_size(size_t* bytes);
+int chemora_grid_export_peer(chemora_grid_t grid, void* record_out);
+int chemora_grid_connect_ipc(chemora_grid_t grid, const void* record_lo, const void* record_hi);
+
+/* ---- testing hooks (not part of the user-facing contract) */
+
+/* Select the stage-kernel variant of this handle: 0 = tiled fast kernel (default),
+ * 1 = one-thread-per-point reference kernel.  Results must be bitwise identical. */
+int chemora_set_kernel_variant(chemora_grid_t grid, int variant);
+
+/* chemora_set_initial without the final halo exchange (ghosts left as cleared/copied). */
+int chemora_set_initial_nofill(chemora_grid_t grid, int kind, const double* host_src,
+                               const double* kind_params, uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* CHEMORA_H */

@@ -1,0 +1,661 @@
+// capi.cpp -- the host runtime behind include/chemora.h: grid handles over a caller-owned
+// workspace, stage sequencing of the RK4 step, the z-slab
+// decomposition and its peer connectivity, and error reporting.
+#include "../../include/chemora.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "grid.hpp"
+#include "kernels.hpp"
+
+using namespace chemora;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(CHEMORA_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+  } while (0)
+
+const double kBenchGauge[10] = {2.0, 1.0, 1.0, 0.0, 1.0, 0.75, 0.0, 1.0, 1.0, 1.0};
+constexpr int kParams = 10;
+
+struct PeerRecord {
+  cudaIpcMemHandle_t handle;
+  uint64_t bytes;
+  int32_t rank, nranks;
+  int64_t local_extent[3];
+  int32_t ghost, n_gf;
+};
+
+}  // namespace
+
+struct chemora_grid_s {
+  chemora_grid_desc desc;
+  double params[kParams];
+  Layout L;
+  int64_t z0;
+  char* ws;
+  size_t ws_bytes;
+  SetPtrs sets;
+  double* dparams;          // device copy of params
+  double* norm_scratch;     // kNormBlocks x len
+  double* norm_out;         // len
+  unsigned long long* nan_flag;
+  unsigned long long* flags;  // [0] written by lo neighbour, [1] by hi neighbour
+  uint64_t step;
+  uint64_t epoch;
+  // z-face neighbours: set bases (same SetId) of the lower / upper slab
+  SetPtrs lo, hi;
+  unsigned long long* lo_flag;  // where WE signal the lower neighbour (its flags[1])
+  unsigned long long* hi_flag;  // where WE signal the upper neighbour (its flags[0])
+  bool ipc;                     // neighbours are other processes (signal through flags)
+  std::vector<void*> opened;    // IPC mappings to close
+  int variant;
+};
+
+namespace {
+
+int n_gf_of(int system) { return system == CHEMORA_SYS_WAVE ? 5 : (system == CHEMORA_SYS_BSSN ? 25 : -1); }
+int radius_of(const chemora_grid_desc& d) {
+  if (d.system == CHEMORA_SYS_WAVE) return (d.fd_order == 0 ? 4 : d.fd_order) / 2;
+  return 3;  // BSSN: lopsided upwind stencils reach 3 points
+}
+
+int validate(const chemora_grid_desc* d) {
+  if (!d) return fail(CHEMORA_E_INVALID, "desc is NULL");
+  const int nf = n_gf_of(d->system);
+  if (nf < 0) return fail(CHEMORA_E_INVALID, "unknown system " + std::to_string(d->system));
+  if (d->n_gf != nf)
+    return fail(CHEMORA_E_INVALID, "n_gf " + std::to_string(d->n_gf) + " does not match the system (" +
+                                       std::to_string(nf) + ")");
+  const int order = d->fd_order == 0 ? 4 : d->fd_order;
+  if (d->system == CHEMORA_SYS_WAVE && !(order == 2 || order == 4 || order == 6 || order == 8))
+    return fail(CHEMORA_E_UNSUPPORTED, "wave fd_order must be 2, 4, 6 or 8");
+  if (d->system == CHEMORA_SYS_BSSN && order != 4)
+    return fail(CHEMORA_E_UNSUPPORTED, "BSSN supports fd_order 4 only");
+  if (d->ghost < radius_of(*d) || d->ghost > 8)
+    return fail(CHEMORA_E_SHAPE, "ghost width " + std::to_string(d->ghost) +
+                                     " must be >= the stencil radius " + std::to_string(radius_of(*d)) +
+                                     " and <= 8");
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks)
+    return fail(CHEMORA_E_INVALID, "bad rank/nranks");
+  for (int a = 0; a < 3; ++a) {
+    if (d->extent[a] < 2 * d->ghost)
+      return fail(CHEMORA_E_SHAPE, "extent[" + std::to_string(a) + "] must be >= 2*ghost");
+    if (!(d->spacing[a] > 0.0) || !std::isfinite(d->spacing[a]))
+      return fail(CHEMORA_E_INVALID, "spacing must be positive");
+  }
+  if (d->extent[0] > (int64_t(1) << 30) || d->extent[1] > (int64_t(1) << 30))
+    return fail(CHEMORA_E_SHAPE, "extent too large");
+  if (d->extent[2] % d->nranks)
+    return fail(CHEMORA_E_SHAPE, "extent[2] must be divisible by nranks");
+  if (d->extent[2] / d->nranks < 2 * d->ghost)
+    return fail(CHEMORA_E_SHAPE, "local slab must have >= 2*ghost planes");
+  if (d->n_params < 0 || (d->n_params > 0 && !d->params) || d->n_params > kParams)
+    return fail(CHEMORA_E_INVALID, "bad params");
+  return CHEMORA_OK;
+}
+
+int norms_len(int system, int n_gf) { return 3 * n_gf + (system == CHEMORA_SYS_WAVE ? 1 : 0); }
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+// workspace: [sets][norm scratch][norm out][params][flags]
+struct WsPlan {
+  size_t sets, scratch, out, params, flags, total;
+};
+WsPlan plan_ws(const Layout& L, int system) {
+  WsPlan p;
+  const int len = norms_len(system, L.n_gf);
+  p.sets = 0;
+  size_t off = align256(sizeof(double) * (size_t)L.gfs * L.n_gf * kNumSets);
+  p.scratch = off;
+  off += align256(sizeof(double) * (size_t)kNormBlocks * len);
+  p.out = off;
+  off += align256(sizeof(double) * len);
+  p.params = off;
+  off += align256(sizeof(double) * kParams);
+  p.flags = off;
+  off += align256(sizeof(unsigned long long) * 4);
+  p.total = off;
+  return p;
+}
+
+Layout layout_of(const chemora_grid_desc& d) {
+  return make_layout(d.extent[0], d.extent[1], d.extent[2] / d.nranks, d.ghost, d.n_gf);
+}
+
+SetPtrs sets_at(char* ws, const Layout& L) {
+  double* base = reinterpret_cast<double*>(ws);
+  SetPtrs s;
+  s.y = base + (size_t)SET_Y * L.n_gf * L.gfs + L.c0;
+  s.q = base + (size_t)SET_Q * L.n_gf * L.gfs + L.c0;
+  s.b = base + (size_t)SET_B * L.n_gf * L.gfs + L.c0;
+  s.c = base + (size_t)SET_C * L.n_gf * L.gfs + L.c0;
+  return s;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_grid(chemora_grid_t g) {
+  if (!g) return fail(CHEMORA_E_INVALID, "grid handle is NULL");
+  return CHEMORA_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------- peer signalling
+// Cross-process slabs: before a phase that reads our ghosts or writes the neighbours'
+// ghost planes, wait until both neighbours have finished the previous phase (their
+// flags, written into OUR memory, reach epoch-1); after it, publish our epoch into theirs.
+// The driver entry points are fetched through the runtime so the library has no link-time
+// dependency on libcuda (it must load on the GPU-less build host).
+typedef CUresult (*PFN_wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+PFN_wait64 g_wait64 = nullptr;
+PFN_write64 g_write64 = nullptr;
+int load_stream_memops() {
+  if (g_wait64 && g_write64) return CHEMORA_OK;
+  cudaDriverEntryPointQueryResult q1, q2;
+  void* f1 = nullptr;
+  void* f2 = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWriteValue64", &f2, cudaEnableDefault, &q2) != cudaSuccess ||
+      !f1 || !f2)
+    return fail(CHEMORA_E_PEER, "stream memory operations are unavailable");
+  g_wait64 = reinterpret_cast<PFN_wait64>(f1);
+  g_write64 = reinterpret_cast<PFN_write64>(f2);
+  return CHEMORA_OK;
+}
+
+int phase_wait(chemora_grid_t g, cudaStream_t st) {
+  if (!g->ipc || g->epoch == 0) return CHEMORA_OK;
+  if (int rc = load_stream_memops()) return rc;
+  const uint64_t want = g->epoch;  // neighbours completed phase `epoch`
+  for (int f = 0; f < 2; ++f) {
+    CUresult r = g_wait64((CUstream)st, (CUdeviceptr)(g->flags + f), want,
+                          CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(CHEMORA_E_PEER, "cuStreamWaitValue64 failed");
+  }
+  return CHEMORA_OK;
+}
+int phase_signal(chemora_grid_t g, cudaStream_t st) {
+  if (!g->ipc) return CHEMORA_OK;
+  if (int rc = load_stream_memops()) return rc;
+  g->epoch += 1;
+  CUresult r1 = g_write64((CUstream)st, (CUdeviceptr)g->lo_flag, g->epoch, 0);
+  CUresult r2 = g_write64((CUstream)st, (CUdeviceptr)g->hi_flag, g->epoch, 0);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+    return fail(CHEMORA_E_PEER, "cuStreamWriteValue64 failed");
+  return CHEMORA_OK;
+}
+
+StageLaunch stage_args(chemora_grid_t g, double dt) {
+  StageLaunch a;
+  a.L = g->L;
+  a.s = g->sets;
+  // output set of stage s: 1 -> B, 2 -> C, 3 -> B, 4 -> y
+  a.img[0] = FaceDst{g->lo.b, g->hi.b};
+  a.img[1] = FaceDst{g->lo.c, g->hi.c};
+  a.img[2] = FaceDst{g->lo.b, g->hi.b};
+  a.img[3] = FaceDst{g->lo.y, g->hi.y};
+  for (int d = 0; d < 3; ++d) a.h[d] = g->desc.spacing[d];
+  a.dt = dt;
+  a.fd_order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
+  a.params = g->dparams;
+  a.nan_flag = g->nan_flag;
+  a.step = g->step;
+  a.k_begin = 0;
+  a.k_end = (int)g->L.nz;
+  a.variant = g->variant;
+  return a;
+}
+
+cudaError_t launch_stage(chemora_grid_t g, const StageLaunch& a, int stage, cudaStream_t st) {
+  return g->desc.system == CHEMORA_SYS_WAVE ? wave_stage(a, stage, st) : bssn_stage(a, stage, st);
+}
+
+int read_nan_flag(chemora_grid_t g, cudaStream_t st) {
+  unsigned long long flag = 0;
+  CUDA_TRY(cudaMemcpyAsync(&flag, g->nan_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (flag != ~0ull) {
+    const unsigned long long step = flag / g->L.n_gf, gf = flag % g->L.n_gf;
+    return fail(CHEMORA_E_NONFINITE, "non-finite value in grid function " + std::to_string(gf) +
+                                         " at step " + std::to_string(step));
+  }
+  return CHEMORA_OK;
+}
+
+cudaMemcpy3DParms copy_params(chemora_grid_t g, int f, double* host, bool to_device, bool padded) {
+  const Layout& L = g->L;
+  const int gh = L.g;
+  cudaMemcpy3DParms p;
+  memset(&p, 0, sizeof(p));
+  const int64_t wx = padded ? L.nx + 2 * gh : L.nx;
+  const int64_t wy = padded ? L.py : L.ny;
+  const int64_t wz = padded ? L.pz : L.nz;
+  double* dbase = g->sets.y + (size_t)f * L.gfs;  // interior origin
+  double* dstart = padded ? dbase - L.c0 + (kXOff - gh) : dbase;
+  // device pitched pointer: rows of px doubles, py rows per plane
+  cudaPitchedPtr dev = make_cudaPitchedPtr(dstart, L.px * sizeof(double), wx * sizeof(double), L.py);
+  double* hbase = host + (size_t)f * wx * wy * wz;
+  cudaPitchedPtr hst = make_cudaPitchedPtr(hbase, wx * sizeof(double), wx * sizeof(double), wy);
+  if (to_device) { p.srcPtr = hst; p.dstPtr = dev; p.kind = cudaMemcpyHostToDevice; }
+  else { p.srcPtr = dev; p.dstPtr = hst; p.kind = cudaMemcpyDeviceToHost; }
+  p.extent = make_cudaExtent(wx * sizeof(double), wy, wz);
+  return p;
+}
+
+int halo_one(chemora_grid_t g, cudaStream_t st) {
+  int rc = phase_wait(g, st);
+  if (rc) return rc;
+  CUDA_TRY(ghost_fill(g->L, g->sets.y, FaceDst{g->lo.y, g->hi.y}, st));
+  return phase_signal(g, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chemora_version(void) { return "chemora-b200 0.1 (sm_100a, fp64)"; }
+
+const char* chemora_last_error(void) { return g_err.c_str(); }
+
+int chemora_norms_len(int32_t system, int32_t n_gf) { return norms_len(system, n_gf); }
+
+int chemora_grid_required_bytes(const chemora_grid_desc* desc, size_t* bytes) {
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!bytes) return fail(CHEMORA_E_INVALID, "bytes is NULL");
+  *bytes = plan_ws(layout_of(*desc), desc->system).total;
+  return CHEMORA_OK;
+}
+
+int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, chemora_grid_t* out) {
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!out) return fail(CHEMORA_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!ws) return fail(CHEMORA_E_INVALID, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(CHEMORA_E_NOMEM, "workspace must be 256-byte aligned");
+  const Layout L = layout_of(*desc);
+  const WsPlan P = plan_ws(L, desc->system);
+  if (bytes < P.total)
+    return fail(CHEMORA_E_NOMEM, "workspace has " + std::to_string(bytes) + " bytes, needs " + std::to_string(P.total));
+  DeviceGuard dg(desc->device);
+  cudaPointerAttributes attr;
+  CUDA_TRY(cudaPointerGetAttributes(&attr, ws));
+  if (attr.type != cudaMemoryTypeDevice || attr.device != desc->device)
+    return fail(CHEMORA_E_INVALID, "workspace is not device memory of desc->device");
+  auto* g = new chemora_grid_s();
+  g->desc = *desc;
+  for (int i = 0; i < kParams; ++i) g->params[i] = kBenchGauge[i];
+  for (int i = 0; i < desc->n_params; ++i) g->params[i] = desc->params[i];
+  g->desc.params = nullptr;
+  g->desc.n_params = kParams;
+  g->L = L;
+  g->z0 = (int64_t)desc->rank * L.nz;
+  g->ws = static_cast<char*>(ws);
+  g->ws_bytes = bytes;
+  g->sets = sets_at(g->ws, L);
+  g->norm_scratch = reinterpret_cast<double*>(g->ws + P.scratch);
+  g->norm_out = reinterpret_cast<double*>(g->ws + P.out);
+  g->dparams = reinterpret_cast<double*>(g->ws + P.params);
+  auto* fl = reinterpret_cast<unsigned long long*>(g->ws + P.flags);
+  g->nan_flag = fl;
+  g->flags = fl + 1;
+  g->step = 0;
+  g->epoch = 0;
+  // a lone slab is its own z neighbour (periodic wrap)
+  g->lo = g->sets;
+  g->hi = g->sets;
+  g->lo_flag = g->flags + 1;
+  g->hi_flag = g->flags;
+  g->ipc = false;
+  g->variant = 0;
+  const char* v = getenv("CHEMORA_KERNEL_VARIANT");
+  if (v) g->variant = atoi(v);
+  unsigned long long init[3] = {~0ull, 0ull, 0ull};
+  cudaError_t e = cudaMemcpy(g->dparams, g->params, sizeof(g->params), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(fl, init, sizeof(init), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(CHEMORA_E_CUDA, std::string("grid_create: ") + cudaGetErrorString(e));
+  }
+  *out = g;
+  return CHEMORA_OK;
+}
+
+int chemora_grid_destroy(chemora_grid_t g) {
+  if (!g) return CHEMORA_OK;
+  {
+    DeviceGuard dg(g->desc.device);
+    for (void* p : g->opened) cudaIpcCloseMemHandle(p);
+  }
+  delete g;
+  return CHEMORA_OK;
+}
+
+int chemora_grid_local(chemora_grid_t g, int64_t* ext, int64_t* z0) {
+  if (int rc = check_grid(g)) return rc;
+  if (ext) { ext[0] = g->L.nx; ext[1] = g->L.ny; ext[2] = g->L.nz; }
+  if (z0) *z0 = g->z0;
+  return CHEMORA_OK;
+}
+
+int chemora_set_kernel_variant(chemora_grid_t g, int variant) {
+  if (int rc = check_grid(g)) return rc;
+  g->variant = variant;
+  return CHEMORA_OK;
+}
+
+static int set_initial_nofill(chemora_grid_t g, int kind, const double* host_src, const double* kp,
+                              uint64_t seed, cudaStream_t st) {
+  DeviceGuard dg(g->desc.device);
+  const Layout& L = g->L;
+  switch (kind) {
+    case CHEMORA_INIT_HOST:
+    case CHEMORA_INIT_HOST_PADDED: {
+      if (!host_src) return fail(CHEMORA_E_INVALID, "host_src is NULL");
+      // the whole y set (ghosts included) is cleared first so unused pad is deterministic
+      CUDA_TRY(cudaMemsetAsync(g->sets.y - L.c0, 0, sizeof(double) * L.gfs * L.n_gf, st));
+      for (int f = 0; f < L.n_gf; ++f) {
+        cudaMemcpy3DParms p = copy_params(g, f, const_cast<double*>(host_src), true,
+                                          kind == CHEMORA_INIT_HOST_PADDED);
+        CUDA_TRY(cudaMemcpy3DAsync(&p, st));
+      }
+      CUDA_TRY(cudaStreamSynchronize(st));  // host_src may be released on return
+      break;
+    }
+    case CHEMORA_INIT_PLANE_WAVES:
+    case CHEMORA_INIT_GAUSSIAN:
+      if (g->desc.system != CHEMORA_SYS_WAVE) return fail(CHEMORA_E_INVALID, "init kind needs the wave system");
+      /* fallthrough */
+    case CHEMORA_INIT_NOISE:
+    case CHEMORA_INIT_MINK_PERT: {
+      if (kind == CHEMORA_INIT_MINK_PERT && g->desc.system != CHEMORA_SYS_BSSN)
+        return fail(CHEMORA_E_INVALID, "MINK_PERT needs the BSSN system");
+      InitArgs a;
+      memset(&a, 0, sizeof(a));
+      a.kind = kind;
+      a.system = g->desc.system;
+      a.seed = seed;
+      a.z0 = g->z0;
+      for (int d = 0; d < 3; ++d) {
+        a.gext[d] = g->desc.extent[d];
+        a.origin[d] = g->desc.origin[d];
+        a.h[d] = g->desc.spacing[d];
+      }
+      if (kind == CHEMORA_INIT_GAUSSIAN) { a.kp[0] = kp ? kp[0] : 1.0; a.kp[1] = kp ? kp[1] : 0.5; }
+      if (kind == CHEMORA_INIT_MINK_PERT) a.kp[0] = kp ? kp[0] : 1e-3;
+      CUDA_TRY(cudaMemsetAsync(g->sets.y - L.c0, 0, sizeof(double) * L.gfs * L.n_gf, st));
+      CUDA_TRY(init_interior(L, g->sets.y, a, st));
+      break;
+    }
+    default:
+      return fail(CHEMORA_E_INVALID, "unknown init kind " + std::to_string(kind));
+  }
+  unsigned long long nf = ~0ull;
+  CUDA_TRY(cudaMemcpyAsync(g->nan_flag, &nf, sizeof(nf), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  g->step = 0;
+  return CHEMORA_OK;
+}
+
+int chemora_set_initial(chemora_grid_t g, int kind, const double* host_src, const double* kp,
+                        uint64_t seed, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (int rc = set_initial_nofill(g, kind, host_src, kp, seed, st)) return rc;
+  if (kind == CHEMORA_INIT_HOST_PADDED) return CHEMORA_OK;
+  DeviceGuard dg(g->desc.device);
+  return halo_one(g, st);
+}
+
+int chemora_set_initial_nofill(chemora_grid_t g, int kind, const double* host_src, const double* kp,
+                               uint64_t seed, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  return set_initial_nofill(g, kind, host_src, kp, seed, as_stream(stream));
+}
+
+static int get_state_impl(chemora_grid_t g, double* host, void* stream, bool padded) {
+  if (int rc = check_grid(g)) return rc;
+  if (!host) return fail(CHEMORA_E_INVALID, "host_dst is NULL");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  for (int f = 0; f < g->L.n_gf; ++f) {
+    cudaMemcpy3DParms p = copy_params(g, f, host, false, padded);
+    CUDA_TRY(cudaMemcpy3DAsync(&p, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return read_nan_flag(g, st);
+}
+
+int chemora_get_state(chemora_grid_t g, double* host, void* stream) {
+  return get_state_impl(g, host, stream, false);
+}
+int chemora_get_state_padded(chemora_grid_t g, double* host, void* stream) {
+  return get_state_impl(g, host, stream, true);
+}
+
+int chemora_rhs(chemora_grid_t g, double* dst, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!dst) return fail(CHEMORA_E_INVALID, "dev_dst is NULL");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  StageLaunch a = stage_args(g, 0.0);
+  if (g->desc.system == CHEMORA_SYS_WAVE) CUDA_TRY(wave_rhs(a, dst, st));
+  else CUDA_TRY(bssn_rhs(a, dst, st));
+  return CHEMORA_OK;
+}
+
+int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (nsteps < 0 || !std::isfinite(dt)) return fail(CHEMORA_E_INVALID, "bad dt or nsteps");
+  if (g->desc.nranks > 1 && !g->ipc && g->lo.y == g->sets.y)
+    return fail(CHEMORA_E_PEER, "multi-slab grid is not connected");
+  if (g->desc.nranks > 1 && !g->ipc)
+    return fail(CHEMORA_E_PEER, "locally connected slabs step through chemora_rk4_step_multi");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  for (int n = 0; n < nsteps; ++n) {
+    StageLaunch a = stage_args(g, dt);
+    for (int s = 1; s <= 4; ++s) {
+      if (int rc = phase_wait(g, st)) return rc;
+      CUDA_TRY(launch_stage(g, a, s, st));
+      if (int rc = phase_signal(g, st)) return rc;
+    }
+    g->step += 1;
+  }
+  return CHEMORA_OK;
+}
+
+int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t nsteps, void* stream) {
+  if (!grids || n < 1) return fail(CHEMORA_E_INVALID, "bad grid list");
+  for (int r = 0; r < n; ++r)
+    if (int rc = check_grid(grids[r])) return rc;
+  if (nsteps < 0 || !std::isfinite(dt)) return fail(CHEMORA_E_INVALID, "bad dt or nsteps");
+  DeviceGuard dg(grids[0]->desc.device);
+  cudaStream_t st = as_stream(stream);
+  for (int step = 0; step < nsteps; ++step) {
+    for (int s = 1; s <= 4; ++s)
+      for (int r = 0; r < n; ++r) {
+        StageLaunch a = stage_args(grids[r], dt);
+        CUDA_TRY(launch_stage(grids[r], a, s, st));
+      }
+    for (int r = 0; r < n; ++r) grids[r]->step += 1;
+  }
+  return CHEMORA_OK;
+}
+
+int chemora_halo_exchange(chemora_grid_t g, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  DeviceGuard dg(g->desc.device);
+  return halo_one(g, as_stream(stream));
+}
+
+int chemora_halo_exchange_multi(chemora_grid_t* grids, int32_t n, void* stream) {
+  if (!grids || n < 1) return fail(CHEMORA_E_INVALID, "bad grid list");
+  DeviceGuard dg(grids[0]->desc.device);
+  cudaStream_t st = as_stream(stream);
+  // per slab: x, y fill then the z push into the neighbours' ghost planes (a push only
+  // writes z-ghost planes, which no other slab's x/y fill touches)
+  for (int r = 0; r < n; ++r) {
+    chemora_grid_t g = grids[r];
+    CUDA_TRY(ghost_fill(g->L, g->sets.y, FaceDst{g->lo.y, g->hi.y}, st));
+  }
+  return CHEMORA_OK;
+}
+
+int chemora_norms_partial(chemora_grid_t g, double* out, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!out) return fail(CHEMORA_E_INVALID, "out is NULL");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  const int len = norms_len(g->desc.system, g->L.n_gf);
+  CUDA_TRY(norms_partial(g->L, g->sets.y, g->desc.system, g->norm_scratch, g->norm_out, st));
+  CUDA_TRY(cudaMemcpyAsync(out, g->norm_out, sizeof(double) * len, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return read_nan_flag(g, st);
+}
+
+int chemora_norms_combine(const chemora_grid_desc* d, const double* partials, int32_t nranks, double* out) {
+  if (!d || !partials || !out || nranks < 1) return fail(CHEMORA_E_INVALID, "bad arguments");
+  const int nf = n_gf_of(d->system);
+  if (nf < 0) return fail(CHEMORA_E_INVALID, "unknown system");
+  const int len = norms_len(d->system, nf);
+  const double vol = d->spacing[0] * d->spacing[1] * d->spacing[2];
+  for (int v = 0; v < len; ++v) {
+    double acc = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+      const double x = partials[(size_t)r * len + v];
+      acc = (v % 3 == 1 && v < 3 * nf) ? std::fmax(acc, x) : acc + x;
+    }
+    if (v < 3 * nf && v % 3 == 0) out[v] = std::sqrt(vol * acc);
+    else if (v < 3 * nf && v % 3 == 1) out[v] = acc;
+    else out[v] = vol * acc;
+  }
+  return CHEMORA_OK;
+}
+
+int chemora_norms(chemora_grid_t g, double* out, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (g->desc.nranks > 1)
+    return fail(CHEMORA_E_UNSUPPORTED, "nranks > 1: gather chemora_norms_partial and call chemora_norms_combine");
+  std::vector<double> part(norms_len(g->desc.system, g->L.n_gf));
+  int rc = chemora_norms_partial(g, part.data(), stream);
+  if (rc && rc != CHEMORA_E_NONFINITE) return rc;
+  int rc2 = chemora_norms_combine(&g->desc, part.data(), 1, out);
+  return rc ? rc : rc2;
+}
+
+int chemora_grid_connect_local(chemora_grid_t* grids, int32_t n) {
+  if (!grids || n < 1) return fail(CHEMORA_E_INVALID, "bad grid list");
+  for (int r = 0; r < n; ++r) {
+    if (int rc = check_grid(grids[r])) return rc;
+    if (grids[r]->desc.rank != r || grids[r]->desc.nranks != n)
+      return fail(CHEMORA_E_PEER, "grids[r] must have rank r of n");
+    if (grids[r]->desc.device != grids[0]->desc.device)
+      return fail(CHEMORA_E_PEER, "local slabs must share one device");
+    if (grids[r]->L.gfs != grids[0]->L.gfs || grids[r]->L.nz != grids[0]->L.nz)
+      return fail(CHEMORA_E_PEER, "slabs have different layouts");
+  }
+  for (int r = 0; r < n; ++r) {
+    chemora_grid_t g = grids[r];
+    g->lo = grids[(r + n - 1) % n]->sets;
+    g->hi = grids[(r + 1) % n]->sets;
+    g->ipc = false;
+  }
+  return CHEMORA_OK;
+}
+
+int chemora_peer_record_size(size_t* bytes) {
+  if (!bytes) return fail(CHEMORA_E_INVALID, "bytes is NULL");
+  *bytes = sizeof(PeerRecord);
+  return CHEMORA_OK;
+}
+
+int chemora_grid_export_peer(chemora_grid_t g, void* rec_out) {
+  if (int rc = check_grid(g)) return rc;
+  if (!rec_out) return fail(CHEMORA_E_INVALID, "record_out is NULL");
+  DeviceGuard dg(g->desc.device);
+  PeerRecord rec;
+  memset(&rec, 0, sizeof(rec));
+  CUDA_TRY(cudaIpcGetMemHandle(&rec.handle, g->ws));
+  rec.bytes = g->ws_bytes;
+  rec.rank = g->desc.rank;
+  rec.nranks = g->desc.nranks;
+  rec.local_extent[0] = g->L.nx; rec.local_extent[1] = g->L.ny; rec.local_extent[2] = g->L.nz;
+  rec.ghost = g->L.g;
+  rec.n_gf = g->L.n_gf;
+  memcpy(rec_out, &rec, sizeof(rec));
+  return CHEMORA_OK;
+}
+
+int chemora_grid_connect_ipc(chemora_grid_t g, const void* rlo, const void* rhi) {
+  if (int rc = check_grid(g)) return rc;
+  if (!rlo || !rhi) return fail(CHEMORA_E_INVALID, "record is NULL");
+  PeerRecord lo, hi;
+  memcpy(&lo, rlo, sizeof(lo));
+  memcpy(&hi, rhi, sizeof(hi));
+  const int n = g->desc.nranks, r = g->desc.rank;
+  if (lo.rank != (r + n - 1) % n || hi.rank != (r + 1) % n || lo.nranks != n || hi.nranks != n)
+    return fail(CHEMORA_E_PEER, "records are not this rank's ring neighbours");
+  for (const PeerRecord* p : {&lo, &hi})
+    if (p->local_extent[0] != g->L.nx || p->local_extent[1] != g->L.ny ||
+        p->local_extent[2] != g->L.nz || p->ghost != g->L.g || p->n_gf != g->L.n_gf)
+      return fail(CHEMORA_E_PEER, "neighbour layout differs");
+  DeviceGuard dg(g->desc.device);
+  const WsPlan P = plan_ws(g->L, g->desc.system);
+  auto open = [&](const PeerRecord& rec, char** base) -> int {
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, rec.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(CHEMORA_E_PEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    g->opened.push_back(p);
+    *base = static_cast<char*>(p);
+    return CHEMORA_OK;
+  };
+  char* blo = nullptr;
+  char* bhi = nullptr;
+  if (int rc = open(lo, &blo)) return rc;
+  if (n == 2) bhi = blo;  // both faces go to the same peer
+  else if (int rc = open(hi, &bhi)) return rc;
+  g->lo = sets_at(blo, g->L);
+  g->hi = sets_at(bhi, g->L);
+  // we signal the lower neighbour in its flags[1] ("from hi") and the upper in flags[0]
+  g->lo_flag = reinterpret_cast<unsigned long long*>(blo + P.flags) + 2;
+  g->hi_flag = reinterpret_cast<unsigned long long*>(bhi + P.flags) + 1;
+  g->ipc = true;
+  g->epoch = 0;
+  return CHEMORA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// device_common.cuh -- small device helpers shared by the stage, ghost and init kernels.
+#pragma once
+#include <cstdint>
+#include "grid.hpp"
+
+namespace chemora {
+
+// Store the periodic ghost images of interior value v at (i, j, k) (PAPER.md:345-347
+// ghost zones).  `own` is the GF array (interior-origin pointer); the
+// z images of the first g planes go to `zlo` at k + nz (the lower neighbour's top ghost
+// planes, or our own when the slab is the whole periodic z range) and those of the last g
+// planes to `zhi` at k - nz.  Every combination of x/y/z images is written so edges and
+// corners equal the doubly/triply wrapped interior value, exactly as the axis-by-axis fill.
+__device__ __forceinline__ void store_images(double* own, double* zlo, double* zhi,
+                                             const Layout& L, int i, int j, int k, double v) {
+  const int g = L.g;
+  const int nx = (int)L.nx, ny = (int)L.ny, nz = (int)L.nz;
+  const int xi = i < g ? i + nx : (i >= nx - g ? i - nx : i);
+  const int yj = j < g ? j + ny : (j >= ny - g ? j - ny : j);
+  const int zk = k < g ? k + nz : (k >= nz - g ? k - nz : k);
+  const bool hx = xi != i, hy = yj != j, hz = zk != k;
+  if (!(hx | hy | hz)) return;
+  double* zb = k < g ? zlo : zhi;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    if (c && !hz) continue;
+    double* base = c ? zb : own;
+    const int64_t kk = c ? zk : k;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (b && !hy) continue;
+      const int64_t jj = b ? yj : j;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        if (a && !hx) continue;
+        if (!(a | b | c)) continue;
+        const int64_t ii = a ? xi : i;
+        base[L.idx(ii, jj, kk)] = v;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool near_face(const Layout& L, int i, int j, int k) {
+  const int g = L.g;
+  return i < g || j < g || k < g || i >= L.nx - g || j >= L.ny - g || k >= L.nz - g;
+}
+
+// Record the first non-finite output: flag = min(step * n_gf + gf).
+__device__ __forceinline__ void check_finite(unsigned long long* flag, unsigned long long code,
+                                             double v) {
+  if (!isfinite(v)) atomicMin(flag, code);
+}
+
+}  // namespace chemora

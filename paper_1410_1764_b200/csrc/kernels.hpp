@@ -1,0 +1,67 @@
+// kernels.hpp -- host-side launch interface between the runtime (capi.cpp) and the
+// CUDA kernels.  Internal; not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "grid.hpp"
+
+namespace chemora {
+
+// Set pointers (interior-origin pointer of GF 0 of a set; GF v = base + v * L.gfs).
+struct SetPtrs {
+  double* y;
+  double* q;
+  double* b;
+  double* c;
+};
+
+// z-face image destinations for the output of one stage: where the images of the first
+// g planes (lo) and of the last g planes (hi) go.  For a whole-z grid both are the output
+// set itself; for a slab they are the neighbours' copies of the same set.
+struct FaceDst {
+  double* lo;
+  double* hi;
+};
+
+struct StageLaunch {
+  Layout L;
+  SetPtrs s;             // this slab's sets
+  FaceDst img[4];        // per stage s=1..4 (index s-1): neighbour/own base of that stage's output set
+  double h[3];
+  double dt;
+  int fd_order;          // wave: 2/4/6/8
+  const double* params;  // device copy of BSSN gauge params (10)
+  unsigned long long* nan_flag;
+  uint64_t step;         // global step index (for the non-finite report)
+  int k_begin, k_end;    // local z-plane range [k_begin, k_end)
+  int variant;           // kernel variant (0 = default fast, 1 = simple reference kernel)
+};
+
+// Wave (Eq. 1) -------------------------------------------------------------------------
+cudaError_t wave_stage(const StageLaunch& a, int stage, cudaStream_t st);
+cudaError_t wave_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
+
+// BSSN (App. A) ------------------------------------------------------------------------
+cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st);
+cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
+
+// Ghost fill of one set (all GFs): x and y locally, then z images stored to face bases.
+cudaError_t ghost_fill(const Layout& L, double* set, FaceDst z, cudaStream_t st);
+
+// Device initial data into the interior of set y (global coordinates).
+struct InitArgs {
+  int kind;
+  int system;
+  uint64_t seed;
+  int64_t gext[3];   // global interior extents
+  int64_t z0;        // global z of local plane 0
+  double origin[3], h[3];
+  double kp[4];      // kind params
+};
+cudaError_t init_interior(const Layout& L, double* set, const InitArgs& a, cudaStream_t st);
+
+// Norm partials of set y: out_dev[len] (deterministic), len = 3 n_gf (+1 wave).
+cudaError_t norms_partial(const Layout& L, const double* set, int system, double* scratch,
+                          double* out_dev, cudaStream_t st);
+
+}  // namespace chemora

@@ -1,0 +1,193 @@
+// wave_stage.cu -- fused RHS + RK4-stage + ghost-image kernels for the first-order scalar
+// wave equation, Eq. 1 (Fig. 1):
+//     d_t u = rho,   d_t rho = delta^ij d_i v_j,   d_t v_i = d_i rho
+// discretised with centered finite differences of order 2W (4th order
+// = W 2 is the default, R2) and advanced by classical RK4 in
+// the one-HBM-pass-per-substage y/Q/B/C arrangement of DESIGN.md §RK4:
+//   stage 1 (in y):  B = y + dt/2 k1
+//   stage 2 (in B):  Q = (y + B)/3 + dt/3 k2 ;  C = y + dt/2 k2 ;  Q.u = dt/6 y.rho + dt/3 B.rho
+//   stage 3 (in C):  B = y + dt k3            ;  Q.u += dt/3 C.rho
+//   stage 4 (in B):  y = Q + B/3 + dt/6 k4    ;  y.u += Q.u + dt/6 B.rho
+// (u is never differentiated, so its stage values are dead and only a carry is kept.)
+// Each stage writes the periodic ghost images of its output (fused boundary fill) and,
+// for a z-slab, stores its boundary planes into the neighbour's ghost planes.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "grid.hpp"
+#include "kernels.hpp"
+#include "device_common.cuh"
+
+namespace chemora {
+namespace {
+
+enum { GU = 0, GRHO = 1, GV1 = 2, GV2 = 3, GV3 = 4 };
+
+// Centered first-derivative weights c_s (s = 1..W) of order 2W: D1 f = sum c_s (f_s - f_-s)/h.
+template <int W> struct D1W;
+template <> struct D1W<1> { static __device__ __forceinline__ double c(int) { return 0.5; } };
+template <> struct D1W<2> {
+  static __device__ __forceinline__ double c(int s) { return s == 1 ? 2.0 / 3.0 : -1.0 / 12.0; }
+};
+template <> struct D1W<3> {
+  static __device__ __forceinline__ double c(int s) {
+    return s == 1 ? 3.0 / 4.0 : (s == 2 ? -3.0 / 20.0 : 1.0 / 60.0);
+  }
+};
+template <> struct D1W<4> {
+  static __device__ __forceinline__ double c(int s) {
+    return s == 1 ? 4.0 / 5.0 : (s == 2 ? -1.0 / 5.0 : (s == 3 ? 4.0 / 105.0 : -1.0 / 280.0));
+  }
+};
+
+template <int W>
+__device__ __forceinline__ double d1(const double* __restrict__ f, int64_t c, int64_t s) {
+  double acc = 0.0;
+#pragma unroll
+  for (int q = W; q >= 1; --q) acc = fma(D1W<W>::c(q), __ldg(f + c + q * s) - __ldg(f + c - q * s), acc);
+  return acc;
+}
+
+struct WaveK {
+  double ih[3];     // 1/h per axis
+  double half, third, sixth, dt, dt2, dt3, dt6;
+};
+
+// RK4 stage update of the 4 differentiated GFs and the u carry, given the stage input
+// centre values S (rho, v1..3 at index 1..4), the RHS k (index 1..4) and krho_u = S.rho.
+// Writes go through `put(gf, value)` for the stage's main output and `putq` for Q.
+template <int STAGE, class Put, class PutQ>
+__device__ __forceinline__ void wave_update(const WaveK& K, const double* S, const double* k,
+                                            const double* Y, const double* Qv, double yu,
+                                            double qu, Put put, PutQ putq) {
+#pragma unroll
+  for (int f = 1; f <= 4; ++f) {
+    if (STAGE == 1) put(f, fma(K.dt2, k[f], Y[f]));
+    if (STAGE == 2) {
+      putq(f, fma(K.dt3, k[f], (Y[f] + S[f]) * K.third));
+      put(f, fma(K.dt2, k[f], Y[f]));
+    }
+    if (STAGE == 3) put(f, fma(K.dt, k[f], Y[f]));
+    if (STAGE == 4) put(f, fma(K.dt6, k[f], fma(S[f], K.third, Qv[f])));
+  }
+  if (STAGE == 2) putq(0, fma(K.dt3, S[1], K.dt6 * Y[1]));
+  if (STAGE == 3) putq(0, fma(K.dt3, S[1], qu));
+  if (STAGE == 4) put(0, fma(K.dt6, S[1], yu + qu));
+}
+
+// ------------------------------------------------------------------ simple kernel
+// One thread per interior point, every stencil operand loaded through the read-only
+// path.  Used for RHS-only evaluation, as the variant-1 reference for tile-independence
+// tests, and as the fallback for shapes the tiled kernel does not take.
+template <int STAGE, int W>
+__global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, double* rhs_dst) {
+  const Layout& L = a.L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = a.k_begin + blockIdx.z;
+  if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
+  const int64_t c = L.idx(i, j, k);
+  const int64_t gfs = L.gfs;
+  const double* in = STAGE == 0 ? a.s.y : (STAGE == 1 ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b)));
+  const double* rho = in + GRHO * gfs;
+  double S[5], kk[5];
+#pragma unroll
+  for (int f = 1; f <= 4; ++f) S[f] = __ldg(in + f * gfs + c);
+  const double dxr = d1<W>(rho, c, 1) * K.ih[0];
+  const double dyr = d1<W>(rho, c, L.px) * K.ih[1];
+  const double dzr = d1<W>(rho, c, L.plane) * K.ih[2];
+  const double dv1 = d1<W>(in + GV1 * gfs, c, 1) * K.ih[0];
+  const double dv2 = d1<W>(in + GV2 * gfs, c, L.px) * K.ih[1];
+  const double dv3 = d1<W>(in + GV3 * gfs, c, L.plane) * K.ih[2];
+  kk[GRHO] = dv1 + dv2 + dv3;
+  kk[GV1] = dxr;
+  kk[GV2] = dyr;
+  kk[GV3] = dzr;
+  if (STAGE == 0) {
+    const int64_t ni = L.nx * L.ny * L.nz;
+    const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
+    rhs_dst[o] = S[GRHO];
+#pragma unroll
+    for (int f = 1; f <= 4; ++f) rhs_dst[f * ni + o] = kk[f];
+    return;
+  }
+  double Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
+  if (STAGE == 2 || STAGE == 3) {
+#pragma unroll
+    for (int f = 1; f <= 4; ++f) Y[f] = a.s.y[f * gfs + c];
+  }
+  if (STAGE == 1) {
+#pragma unroll
+    for (int f = 1; f <= 4; ++f) Y[f] = S[f];
+  }
+  if (STAGE == 3) qu = a.s.q[c];
+  if (STAGE == 4) {
+#pragma unroll
+    for (int f = 1; f <= 4; ++f) Qv[f] = a.s.q[f * gfs + c];
+    qu = a.s.q[c];
+    yu = a.s.y[c];
+  }
+  double* out = STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y));
+  const FaceDst fd = a.img[STAGE > 0 ? STAGE - 1 : 0];
+  const bool nf = near_face(L, i, j, k);
+  const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
+  auto put = [&](int f, double v) {
+    out[f * gfs + c] = v;
+    if (nf) store_images(out + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+    if (STAGE == 4) check_finite(a.nan_flag, code0 + f, v);
+  };
+  auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
+  wave_update<STAGE>(K, S, kk, Y, Qv, yu, qu, put, putq);
+}
+
+template <int STAGE, int W>
+cudaError_t launch_simple(const StageLaunch& a, const WaveK& K, double* dst, cudaStream_t st) {
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  dim3 block(32, 8, 1);
+  dim3 grid((unsigned)((a.L.nx + 31) / 32), (unsigned)((a.L.ny + 7) / 8), (unsigned)nk);
+  wave_simple<STAGE, W><<<grid, block, 0, st>>>(a, K, dst);
+  return cudaGetLastError();
+}
+
+WaveK make_k(const StageLaunch& a) {
+  WaveK K;
+  for (int d = 0; d < 3; ++d) K.ih[d] = 1.0 / a.h[d];
+  K.half = 0.5; K.third = 1.0 / 3.0; K.sixth = 1.0 / 6.0;
+  K.dt = a.dt; K.dt2 = a.dt / 2.0; K.dt3 = a.dt / 3.0; K.dt6 = a.dt / 6.0;
+  return K;
+}
+
+template <int W>
+cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
+  const WaveK K = make_k(a);
+  switch (stage) {
+    case 0: return launch_simple<0, W>(a, K, dst, st);
+    case 1: return launch_simple<1, W>(a, K, dst, st);
+    case 2: return launch_simple<2, W>(a, K, dst, st);
+    case 3: return launch_simple<3, W>(a, K, dst, st);
+    case 4: return launch_simple<4, W>(a, K, dst, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t dispatch(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
+  switch (a.fd_order) {
+    case 2: return dispatch_stage<1>(a, stage, dst, st);
+    case 4: return dispatch_stage<2>(a, stage, dst, st);
+    case 6: return dispatch_stage<3>(a, stage, dst, st);
+    case 8: return dispatch_stage<4>(a, stage, dst, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t wave_stage(const StageLaunch& a, int stage, cudaStream_t st) {
+  return dispatch(a, stage, nullptr, st);
+}
+
+cudaError_t wave_rhs(const StageLaunch& a, double* dst, cudaStream_t st) {
+  return dispatch(a, 0, dst, st);
+}
+
+}  // namespace chemora
