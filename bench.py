@@ -46,7 +46,7 @@ def measured_peaks():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    def __init__(self, index=0, period_ms=200):
+    def __init__(self, index=0, period_ms=100):
         self.index, self.period = index, period_ms
         self.proc = None
         self.lines = []
@@ -172,12 +172,13 @@ def workload(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chemora", choices=["chemora", "reference"])
     ap.add_argument("--config", default="wave512", choices=["wave512", "bssn192"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--variant", type=int, default=None, help="stage-kernel variant (testing)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -202,6 +203,8 @@ def main():
     h = (L / n[0], L / n[1], L / n[2])
     dt = 0.25 * min(h)
     g = P.Grid(system, gext, h, device=local, rank=rank, nranks=world)
+    if args.variant is not None:
+        g.set_kernel_variant(args.variant)
     if world > 1:
         g.connect_ipc()
     init = C.INIT_PLANE_WAVES if system == C.SYS_WAVE else C.INIT_MINK_PERT

@@ -17,6 +17,9 @@ ROOT = os.path.dirname(HERE)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+# the wave kernels exist in two tilings that must agree bitwise: no implicit FMA
+# contraction there (every fma is explicit in the source)
+NO_FMAD = {"wave_stage.cu"}
 SOURCES = ["wave_stage.cu", "bssn_stage.cu", "ghost_init_norms.cu", "capi.cpp"]
 
 
@@ -32,6 +35,8 @@ def _compile(src: str, verbose: bool) -> str:
     cmd = ["nvcc", *ARCH, *NVFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cpp"):
         cmd = ["nvcc", "-x", "cu", *cmd[1:]]
+    if src in NO_FMAD:
+        cmd.insert(1, "-fmad=false")
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(OBJ, os.path.basename(src) + ".log")
     with open(log, "w") as fh:

@@ -139,6 +139,109 @@ __global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, doubl
   wave_update<STAGE>(K, S, kk, Y, Qv, yu, qu, put, putq);
 }
 
+// ------------------------------------------------------------------ z-march kernel
+// 2.5-D: a CTA owns a BX x BY column tile of the x-y plane and marches up a chunk of z
+// planes.  The z-stencil operands (rho and v3, the only GFs differentiated along z) live in
+// a (2W+1)-deep register queue per thread, so every plane of them is loaded from HBM once;
+// x/y neighbours come through L1 (the CTA's own rows) or L2 (tile halos).  Arithmetic is
+// instruction-for-instruction that of wave_simple (bitwise identical results).
+template <int STAGE, int W, int BX, int BY>
+__global__ void __launch_bounds__(BX * BY) wave_zmarch(StageLaunch a, WaveK K, int kchunk) {
+  const Layout& L = a.L;
+  const int i = blockIdx.x * BX + threadIdx.x;
+  const int j = blockIdx.y * BY + threadIdx.y;
+  const int kb = a.k_begin + blockIdx.z * kchunk;
+  const int ke = min(kb + kchunk, a.k_end);
+  if (i >= L.nx || j >= L.ny || kb >= ke) return;
+  const int64_t gfs = L.gfs, px = L.px, pl = L.plane;
+  const double* in = STAGE == 1 ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b));
+  const double* __restrict__ rho = in + GRHO * gfs;
+  const double* __restrict__ v1 = in + GV1 * gfs;
+  const double* __restrict__ v2 = in + GV2 * gfs;
+  const double* __restrict__ v3 = in + GV3 * gfs;
+  double* out = STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y));
+  const FaceDst fd = a.img[STAGE - 1];
+  const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
+  int64_t c = L.idx(i, j, kb);
+  double qr[2 * W + 1], qw[2 * W + 1];
+#pragma unroll
+  for (int q = 0; q < 2 * W; ++q) {
+    qr[q] = __ldg(rho + c + (q - W) * pl);
+    qw[q] = __ldg(v3 + c + (q - W) * pl);
+  }
+  for (int k = kb; k < ke; ++k, c += pl) {
+    qr[2 * W] = __ldg(rho + c + W * pl);
+    qw[2 * W] = __ldg(v3 + c + W * pl);
+    double S[5], kk[5];
+    S[GRHO] = qr[W];
+    S[GV1] = __ldg(v1 + c);
+    S[GV2] = __ldg(v2 + c);
+    S[GV3] = qw[W];
+    double dzr = 0.0, dv3 = 0.0;
+#pragma unroll
+    for (int q = W; q >= 1; --q) {
+      dzr = fma(D1W<W>::c(q), qr[W + q] - qr[W - q], dzr);
+      dv3 = fma(D1W<W>::c(q), qw[W + q] - qw[W - q], dv3);
+    }
+    const double dxr = d1<W>(rho, c, 1) * K.ih[0];
+    const double dyr = d1<W>(rho, c, px) * K.ih[1];
+    dzr = dzr * K.ih[2];
+    const double dv1 = d1<W>(v1, c, 1) * K.ih[0];
+    const double dv2 = d1<W>(v2, c, px) * K.ih[1];
+    dv3 = dv3 * K.ih[2];
+    kk[GRHO] = dv1 + dv2 + dv3;
+    kk[GV1] = dxr;
+    kk[GV2] = dyr;
+    kk[GV3] = dzr;
+    double Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
+    if (STAGE == 2 || STAGE == 3) {
+#pragma unroll
+      for (int f = 1; f <= 4; ++f) Y[f] = a.s.y[f * gfs + c];
+    }
+    if (STAGE == 1) {
+#pragma unroll
+      for (int f = 1; f <= 4; ++f) Y[f] = S[f];
+    }
+    if (STAGE == 3) qu = a.s.q[c];
+    if (STAGE == 4) {
+#pragma unroll
+      for (int f = 1; f <= 4; ++f) Qv[f] = a.s.q[f * gfs + c];
+      qu = a.s.q[c];
+      yu = a.s.y[c];
+    }
+    const bool nf = near_face(L, i, j, k);
+    auto put = [&](int f, double v) {
+      out[f * gfs + c] = v;
+      if (nf) store_images(out + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+      if (STAGE == 4) check_finite(a.nan_flag, code0 + f, v);
+    };
+    auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
+    wave_update<STAGE>(K, S, kk, Y, Qv, yu, qu, put, putq);
+#pragma unroll
+    for (int q = 0; q < 2 * W; ++q) {
+      qr[q] = qr[q + 1];
+      qw[q] = qw[q + 1];
+    }
+  }
+}
+
+template <int STAGE, int W>
+cudaError_t launch_zmarch(const StageLaunch& a, const WaveK& K, cudaStream_t st) {
+  constexpr int BX = 32, BY = 8;
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  const int64_t tiles = ((a.L.nx + BX - 1) / BX) * ((a.L.ny + BY - 1) / BY);
+  // enough CTAs for ~4 waves of 148 SMs x 4 resident CTAs, but chunks of >= 8 planes
+  int64_t want = (4 * 148 * 4 + tiles - 1) / tiles;
+  int chunk = (int)((nk + want - 1) / want);
+  if (chunk < 8) chunk = 8;
+  if (chunk > nk) chunk = nk;
+  const int nchunks = (nk + chunk - 1) / chunk;
+  dim3 grid((unsigned)((a.L.nx + BX - 1) / BX), (unsigned)((a.L.ny + BY - 1) / BY), (unsigned)nchunks);
+  wave_zmarch<STAGE, W, BX, BY><<<grid, dim3(BX, BY, 1), 0, st>>>(a, K, chunk);
+  return cudaGetLastError();
+}
+
 template <int STAGE, int W>
 cudaError_t launch_simple(const StageLaunch& a, const WaveK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
@@ -160,6 +263,14 @@ WaveK make_k(const StageLaunch& a) {
 template <int W>
 cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
   const WaveK K = make_k(a);
+  if (a.variant == 0) {
+    switch (stage) {
+      case 1: return launch_zmarch<1, W>(a, K, st);
+      case 2: return launch_zmarch<2, W>(a, K, st);
+      case 3: return launch_zmarch<3, W>(a, K, st);
+      case 4: return launch_zmarch<4, W>(a, K, st);
+    }
+  }
   switch (stage) {
     case 0: return launch_simple<0, W>(a, K, dst, st);
     case 1: return launch_simple<1, W>(a, K, dst, st);
