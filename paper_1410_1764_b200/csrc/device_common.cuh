@@ -11,10 +11,11 @@ namespace chemora {
 // planes, or our own when the slab is the whole periodic z range) and those of the last g
 // planes to `zhi` at k - nz.  Every combination of x/y/z images is written so edges and
 // corners equal the doubly/triply wrapped interior value, exactly as the axis-by-axis fill.
-__device__ __forceinline__ void store_images(double* own, double* zlo, double* zhi,
-                                             const Layout& L, int i, int j, int k, double v) {
-  const int g = L.g;
-  const int nx = (int)L.nx, ny = (int)L.ny, nz = (int)L.nz;
+// Out of line: only threads near a face call it, and keeping its index arithmetic out of
+// the stage kernels' register allocation is worth the call.
+__device__ __noinline__ void store_images_n(double* own, double* zlo, double* zhi, int nx, int ny,
+                                            int nz, int g, int64_t px, int64_t plane, int i, int j,
+                                            int k, double v) {
   const int xi = i < g ? i + nx : (i >= nx - g ? i - nx : i);
   const int yj = j < g ? j + ny : (j >= ny - g ? j - ny : j);
   const int zk = k < g ? k + nz : (k >= nz - g ? k - nz : k);
@@ -35,10 +36,14 @@ __device__ __forceinline__ void store_images(double* own, double* zlo, double* z
         if (a && !hx) continue;
         if (!(a | b | c)) continue;
         const int64_t ii = a ? xi : i;
-        base[L.idx(ii, jj, kk)] = v;
+        base[kk * plane + jj * px + ii] = v;
       }
     }
   }
+}
+__device__ __forceinline__ void store_images(double* own, double* zlo, double* zhi,
+                                             const Layout& L, int i, int j, int k, double v) {
+  store_images_n(own, zlo, zhi, (int)L.nx, (int)L.ny, (int)L.nz, L.g, L.px, L.plane, i, j, k, v);
 }
 
 __device__ __forceinline__ bool near_face(const Layout& L, int i, int j, int k) {

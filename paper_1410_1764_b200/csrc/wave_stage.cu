@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, doubl
 // x/y neighbours come through L1 (the CTA's own rows) or L2 (tile halos).  Arithmetic is
 // instruction-for-instruction that of wave_simple (bitwise identical results).
 template <int STAGE, int W, int BX, int BY>
-__global__ void __launch_bounds__(BX * BY) wave_zmarch(StageLaunch a, WaveK K, int kchunk) {
+__global__ void __launch_bounds__(BX * BY, 4) wave_zmarch(StageLaunch a, WaveK K, int kchunk) {
   const Layout& L = a.L;
   const int i = blockIdx.x * BX + threadIdx.x;
   const int j = blockIdx.y * BY + threadIdx.y;
@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(BX * BY) wave_zmarch(StageLaunch a, WaveK K, i
     qr[q] = __ldg(rho + c + (q - W) * pl);
     qw[q] = __ldg(v3 + c + (q - W) * pl);
   }
+#pragma unroll 1
   for (int k = kb; k < ke; ++k, c += pl) {
     qr[2 * W] = __ldg(rho + c + W * pl);
     qw[2 * W] = __ldg(v3 + c + W * pl);
@@ -263,7 +264,8 @@ WaveK make_k(const StageLaunch& a) {
 template <int W>
 cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
   const WaveK K = make_k(a);
-  if (a.variant == 0) {
+  // variant 0 (default) and 1: one thread per point; 2: register-queue z-march
+  if (a.variant == 2) {
     switch (stage) {
       case 1: return launch_zmarch<1, W>(a, K, st);
       case 2: return launch_zmarch<2, W>(a, K, st);
