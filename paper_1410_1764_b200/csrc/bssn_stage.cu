@@ -1,8 +1,445 @@
-// bssn_stage.cu -- BSSN fused stage kernels.  Not yet implemented.
+// bssn_stage.cu -- fused RHS + RK4-stage + ghost-image kernels for the 25-GF BSSN-like
+// Einstein system ("the Einstein equations ...
+// several thousand floating point operations to evaluate the RHS at a single grid
+// point"; reading R7), 4th-order centered D1/D2/mixed stencils and 4th-order
+// lopsided upwind advection (R6), advanced by the same one-pass y/Q/B/C RK4
+// arrangement as the wave kernels (every BSSN GF is a stencil input):
+//   stage 1 (in y): B = y + dt/2 k1
+//   stage 2 (in B): Q = (y + B)/3 + dt/3 k2 ; C = y + dt/2 k2
+//   stage 3 (in C): B = y + dt k3
+//   stage 4 (in B): y = Q + B/3 + dt/6 k4
+//
+// The RHS is written on symmetric-packed tensors (xx, xy, xz, yy, yz, zz) with the
+// advection term evaluated branch-free as beta * S f + |beta| * A f, where
+// S = (D+ + D-)/2 and A = (D+ - D-)/2 (identical to max(beta,0) D+ + min(beta,0) D-).
 #include <cuda_runtime.h>
+#include <cstdint>
+#include "grid.hpp"
 #include "kernels.hpp"
+#include "device_common.cuh"
 
 namespace chemora {
-cudaError_t bssn_stage(const StageLaunch&, int, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t bssn_rhs(const StageLaunch&, double*, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+enum {
+  V_PHI = 0, V_GT = 1, V_TRK = 7, V_AT = 8, V_XT = 14, V_ALPHA = 17, V_AUX = 18, V_BETA = 19,
+  V_B = 22, NV = 25
+};
+
+// packed index of the symmetric pair (i, j)
+__host__ __device__ constexpr int sy(int i, int j) {
+  return i == j ? (i == 0 ? 0 : (i == 1 ? 3 : 5)) : (i + j == 1 ? 1 : (i + j == 2 ? 2 : 4));
+}
+// multiplicity of a packed symmetric index in a full contraction (1 diagonal, 2 off)
+__host__ __device__ constexpr double mult(int s) { return (s == 0 || s == 3 || s == 5) ? 1.0 : 2.0; }
+__host__ __device__ constexpr int sI(int s) { return s == 0 ? 0 : (s == 1 ? 0 : (s == 2 ? 0 : (s == 3 ? 1 : (s == 4 ? 1 : 2)))); }
+__host__ __device__ constexpr int sJ(int s) { return s == 0 ? 0 : (s == 1 ? 1 : (s == 2 ? 2 : (s == 3 ? 1 : (s == 4 ? 2 : 2)))); }
+
+struct BssnK {
+  double i12h[3];     // 1/(12 h_a)
+  double i12h2[3];    // 1/(12 h_a^2)
+  double i144hh[3];   // 1/(144 h_a h_b) for the pairs (xy, xz, yz) -> index a+b-1
+  double i24h[3];     // 1/(24 h_a)
+  double dt, dt2, dt3, dt6, third;
+  double F_alpha, n_alpha, L, eta_alpha, c_alpha_adv, C_beta, p_beta, S_B, eta, c_beta_adv;
+};
+
+struct Strides {
+  int64_t s[3];
+};
+
+__device__ __forceinline__ double ld(const double* __restrict__ p) { return __ldg(p); }
+
+// centered 4th-order D1 (without the 1/(12h) factor)
+__device__ __forceinline__ double D1raw(const double* __restrict__ f, int64_t c, int64_t s) {
+  return 8.0 * (ld(f + c + s) - ld(f + c - s)) - (ld(f + c + 2 * s) - ld(f + c - 2 * s));
+}
+// centered 4th-order D2 (without 1/(12h^2)), given the centre value
+__device__ __forceinline__ double D2raw(const double* __restrict__ f, int64_t c, int64_t s, double f0) {
+  return 16.0 * (ld(f + c + s) + ld(f + c - s)) - (ld(f + c + 2 * s) + ld(f + c - 2 * s)) - 30.0 * f0;
+}
+// mixed D1_a D1_b (without 1/(144 h_a h_b))
+__device__ __forceinline__ double D11raw(const double* __restrict__ f, int64_t c, int64_t sa, int64_t sb) {
+  const double p1 = D1raw(f, c + sa, sb), m1 = D1raw(f, c - sa, sb);
+  const double p2 = D1raw(f, c + 2 * sa, sb), m2 = D1raw(f, c - 2 * sa, sb);
+  return 8.0 * (p1 - m1) - (p2 - m2);
+}
+// upwind advection along one axis: beta * S f + |beta| * A f (without 1/(24h))
+__device__ __forceinline__ double ADVraw(const double* __restrict__ f, int64_t c, int64_t s, double f0, double beta) {
+  const double a1 = ld(f + c + s), b1 = ld(f + c - s);
+  const double a2 = ld(f + c + 2 * s), b2 = ld(f + c - 2 * s);
+  const double a3 = ld(f + c + 3 * s), b3 = ld(f + c - 3 * s);
+  const double S = 21.0 * (a1 - b1) - 6.0 * (a2 - b2) + (a3 - b3);
+  const double A = 15.0 * (a1 + b1) - 6.0 * (a2 + b2) + (a3 + b3) - 20.0 * f0;
+  return fma(beta, S, fabs(beta) * A);
+}
+
+__device__ __forceinline__ double adv(const double* __restrict__ f, int64_t c, const Strides& st,
+                                      const double* beta, double f0, const BssnK& K) {
+  double r = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) r = fma(ADVraw(f, c, st.s[a], f0, beta[a]), K.i24h[a], r);
+  return r;
+}
+
+// Evaluate the 25 right-hand sides at interior offset c of the input set `in`.
+// (Advection terms included.)  App. A.2-A.3.
+__device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_t gfs, int64_t c,
+                                           const Strides& st, const BssnK& K, double* rhs) {
+  auto F = [&](int v) { return in + v * gfs; };
+  // ---- point values
+  double gt[6], At[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) { gt[s] = ld(F(V_GT + s) + c); At[s] = ld(F(V_AT + s) + c); }
+  const double phi = ld(F(V_PHI) + c), trK = ld(F(V_TRK) + c), alpha = ld(F(V_ALPHA) + c);
+  const double Aux = ld(F(V_AUX) + c);
+  double Xt[3], beta[3], Bv[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    Xt[i] = ld(F(V_XT + i) + c); beta[i] = ld(F(V_BETA + i) + c); Bv[i] = ld(F(V_B + i) + c);
+  }
+  // ---- inverse conformal metric gu = adj(gt) / det(gt)
+  const double c00 = gt[3] * gt[5] - gt[4] * gt[4];
+  const double c01 = gt[2] * gt[4] - gt[1] * gt[5];
+  const double c02 = gt[1] * gt[4] - gt[2] * gt[3];
+  const double det = gt[0] * c00 + gt[1] * c01 + gt[2] * c02;
+  const double idet = 1.0 / det;
+  double gu[6];
+  gu[0] = c00 * idet;
+  gu[1] = c01 * idet;
+  gu[2] = c02 * idet;
+  gu[3] = (gt[0] * gt[5] - gt[2] * gt[2]) * idet;
+  gu[4] = (gt[1] * gt[2] - gt[0] * gt[4]) * idet;
+  gu[5] = (gt[0] * gt[3] - gt[1] * gt[1]) * idet;
+  const double em4phi = exp(-4.0 * phi);
+
+  // ---- first derivatives of the metric -> Christoffels (first kind Gl, second kind Gu)
+  double Gl[3][6];  // Gl[i][s(j,k)] = 1/2 (d_j gt_ik + d_k gt_ij - d_i gt_jk)
+  {
+    double dg[3][6];
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+      for (int s = 0; s < 6; ++s) dg[l][s] = D1raw(F(V_GT + s), c, st.s[l]) * K.i12h[l];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int j = sI(s), k = sJ(s);
+        Gl[i][s] = 0.5 * (dg[j][sy(i, k)] + dg[k][sy(i, j)] - dg[i][s]);
+      }
+  }
+  double Gu[3][6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      Gu[i][s] = gu[sy(i, 0)] * Gl[0][s] + gu[sy(i, 1)] * Gl[1][s] + gu[sy(i, 2)] * Gl[2][s];
+  double Xtn[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) a = fma(mult(s) * gu[s], Gu[i][s], a);
+    Xtn[i] = a;
+  }
+  // ---- other first derivatives
+  double dphi[3], dalpha[3], dtrK[3], dbeta[3][3], dXt[3][3];  // dbeta[l][k] = d_l beta^k
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    dphi[l] = D1raw(F(V_PHI), c, st.s[l]) * K.i12h[l];
+    dalpha[l] = D1raw(F(V_ALPHA), c, st.s[l]) * K.i12h[l];
+    dtrK[l] = D1raw(F(V_TRK), c, st.s[l]) * K.i12h[l];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dbeta[l][k] = D1raw(F(V_BETA + k), c, st.s[l]) * K.i12h[l];
+      dXt[l][k] = D1raw(F(V_XT + k), c, st.s[l]) * K.i12h[l];
+    }
+  }
+  // ---- conformal Ricci tensor R~_ij
+  double Rt[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) Rt[s] = 0.0;
+  // -1/2 gu^lm d_l d_m gt_ij, pair (l,m) at a time
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    const int l = sI(p), m = sJ(p);
+    const double w = -0.5 * mult(p) * gu[p];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const double* f = F(V_GT + s);
+      const double dd = (l == m) ? D2raw(f, c, st.s[l], gt[s]) * K.i12h2[l]
+                                 : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
+      Rt[s] = fma(w, dd, Rt[s]);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    double r = Rt[s];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      r = fma(0.5 * gt[sy(k, i)], dXt[j][k], r);
+      r = fma(0.5 * gt[sy(k, j)], dXt[i][k], r);
+      r = fma(0.5 * Xtn[k], Gl[i][sy(j, k)] + Gl[j][sy(i, k)], r);
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          t = fma(Gu[k][sy(l, i)], Gl[j][sy(k, m)], t);
+          t = fma(Gu[k][sy(l, j)], Gl[i][sy(k, m)], t);
+          t = fma(Gu[k][sy(i, m)], Gl[k][sy(l, j)], t);
+        }
+        r = fma(gu[sy(l, m)], t, r);
+      }
+    Rt[s] = r;
+  }
+  // ---- phi terms: D~_i D~_j phi, traces
+  double DDphi[6], DDalpha[6];
+  double ddalpha[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    const double ddp = (i == j) ? D2raw(F(V_PHI), c, st.s[i], phi) * K.i12h2[i]
+                                : D11raw(F(V_PHI), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
+    const double dda = (i == j) ? D2raw(F(V_ALPHA), c, st.s[i], alpha) * K.i12h2[i]
+                                : D11raw(F(V_ALPHA), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
+    ddalpha[s] = dda;
+    DDphi[s] = ddp - (Gu[0][s] * dphi[0] + Gu[1][s] * dphi[1] + Gu[2][s] * dphi[2]);
+  }
+  double gudphi[3];  // gt^kl d_l phi
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gudphi[k] = gu[sy(k, 0)] * dphi[0] + gu[sy(k, 1)] * dphi[1] + gu[sy(k, 2)] * dphi[2];
+  double trDDphi = 0.0, dphi2 = 0.0;
+#pragma unroll
+  for (int s = 0; s < 6; ++s) trDDphi = fma(mult(s) * gu[s], DDphi[s], trDDphi);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dphi2 = fma(gudphi[k], dphi[k], dphi2);
+  // D_i D_j alpha with the physical Christoffel
+  // Gamma^k_ij = Gu^k_ij + 2 (delta^k_i d_j phi + delta^k_j d_i phi - gt_ij gt^kl d_l phi)
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    double gam_da = Gu[0][s] * dalpha[0] + Gu[1][s] * dalpha[1] + Gu[2][s] * dalpha[2];
+    const double gdpda = gudphi[0] * dalpha[0] + gudphi[1] * dalpha[1] + gudphi[2] * dalpha[2];
+    gam_da += 2.0 * (dalpha[i] * dphi[j] + dalpha[j] * dphi[i] - gt[s] * gdpda);
+    DDalpha[s] = ddalpha[s] - gam_da;
+  }
+  double trDDalpha;
+  {
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) s1 = fma(mult(s) * gu[s], ddalpha[s], s1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { s2 = fma(Xtn[k], dalpha[k], s2); s3 = fma(gudphi[k], dalpha[k], s3); }
+    trDDalpha = em4phi * (s1 - s2 + 2.0 * s3);
+  }
+  // ---- R_ij = R~_ij + R^phi_ij ; X_ij = -D_i D_j alpha + alpha R_ij
+  double X[6], trX = 0.0;
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    const double Rphi = -2.0 * DDphi[s] - 2.0 * gt[s] * trDDphi + 4.0 * dphi[i] * dphi[j] - 4.0 * gt[s] * dphi2;
+    X[s] = fma(alpha, Rt[s] + Rphi, -DDalpha[s]);
+    trX = fma(mult(s) * gu[s], X[s], trX);
+  }
+  // ---- raised At: Am[i][j] = At^i_j (full 3x3), Au = At^ij (sym)
+  double Am[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      Am[i][j] = gu[sy(i, 0)] * At[sy(0, j)] + gu[sy(i, 1)] * At[sy(1, j)] + gu[sy(i, 2)] * At[sy(2, j)];
+  double Au[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    Au[s] = Am[i][0] * gu[sy(0, j)] + Am[i][1] * gu[sy(1, j)] + Am[i][2] * gu[sy(2, j)];
+  }
+  double AA = 0.0;
+#pragma unroll
+  for (int s = 0; s < 6; ++s) AA = fma(mult(s) * At[s], Au[s], AA);
+  const double divb = dbeta[0][0] + dbeta[1][1] + dbeta[2][2];
+
+  // ---- RHS (without advection; added below)
+  rhs[V_PHI] = (divb - alpha * trK) * (1.0 / 6.0);
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    double rg = -2.0 * alpha * At[s] - (2.0 / 3.0) * gt[s] * divb;
+    double ra = em4phi * (X[s] - (1.0 / 3.0) * gt[s] * trX) - (2.0 / 3.0) * At[s] * divb;
+    double aam = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      rg = fma(gt[sy(i, k)], dbeta[j][k], rg);
+      rg = fma(gt[sy(j, k)], dbeta[i][k], rg);
+      ra = fma(At[sy(i, k)], dbeta[j][k], ra);
+      ra = fma(At[sy(j, k)], dbeta[i][k], ra);
+      aam = fma(At[sy(i, k)], Am[k][j], aam);
+    }
+    ra = fma(alpha, trK * At[s] - 2.0 * aam, ra);
+    rhs[V_GT + s] = rg;
+    rhs[V_AT + s] = ra;
+  }
+  const double rhs_trK_noadv = -trDDalpha + alpha * (AA + trK * trK * (1.0 / 3.0));
+  rhs[V_TRK] = rhs_trK_noadv;
+  // Xt: needs second derivatives of beta
+  double ddivb[3] = {0.0, 0.0, 0.0};  // d_j (d . beta)
+  double lapb[3] = {0.0, 0.0, 0.0};   // gt^jk d_j d_k beta^i
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    const int l = sI(p), m = sJ(p);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double* f = F(V_BETA + i);
+      const double dd = (l == m) ? D2raw(f, c, st.s[l], beta[i]) * K.i12h2[l]
+                                 : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
+      lapb[i] = fma(mult(p) * gu[p], dd, lapb[i]);
+      // d_l d_m beta^i contributes to d_j(d.beta) for (j = l, i = m) and (j = m, i = l)
+      if (i == m) ddivb[l] += dd;
+      if (i == l && l != m) ddivb[m] += dd;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double r = lapb[i] + (1.0 / 3.0) * (gu[sy(i, 0)] * ddivb[0] + gu[sy(i, 1)] * ddivb[1] + gu[sy(i, 2)] * ddivb[2]);
+    r = fma((2.0 / 3.0) * Xtn[i], divb, r);
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      r = fma(-Xtn[j], dbeta[j][i], r);
+      r = fma(-2.0 * Au[sy(i, j)], dalpha[j], r);
+      s = fma(6.0 * Au[sy(i, j)], dphi[j], s);
+      s = fma(-(2.0 / 3.0) * gu[sy(i, j)], dtrK[j], s);
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) s = fma(mult(q) * Gu[i][q], Au[q], s);
+    rhs[V_XT + i] = fma(2.0 * alpha, s, r);
+  }
+  // ---- advection of every GF, and the gauge equations (App. A.3)
+  double advv[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double f0;
+    if (v == V_PHI) f0 = phi;
+    else if (v >= V_GT && v < V_GT + 6) f0 = gt[v - V_GT];
+    else if (v == V_TRK) f0 = trK;
+    else if (v >= V_AT && v < V_AT + 6) f0 = At[v - V_AT];
+    else if (v >= V_XT && v < V_XT + 3) f0 = Xt[v - V_XT];
+    else if (v == V_ALPHA) f0 = alpha;
+    else if (v == V_AUX) f0 = Aux;
+    else if (v >= V_BETA && v < V_BETA + 3) f0 = beta[v - V_BETA];
+    else f0 = Bv[v - V_B];
+    advv[v] = adv(F(v), c, st, beta, f0, K);
+  }
+#pragma unroll
+  for (int v = 0; v < V_ALPHA; ++v) rhs[v] += advv[v];
+  const double rhs_trK = rhs[V_TRK];
+  const double apow_n = (K.n_alpha == 1.0) ? alpha : pow(alpha, K.n_alpha);
+  rhs[V_ALPHA] = -K.F_alpha * apow_n * (K.L * Aux + (1.0 - K.L) * trK) + K.c_alpha_adv * advv[V_ALPHA];
+  rhs[V_AUX] = K.L * (rhs_trK - K.eta_alpha * Aux) + K.c_alpha_adv * advv[V_AUX];
+  const double apow_p = (K.p_beta == 0.0) ? 1.0 : pow(alpha, K.p_beta);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    rhs[V_BETA + i] = K.C_beta * apow_p * (K.S_B * Bv[i] + (1.0 - K.S_B) * (Xt[i] - K.eta * beta[i])) +
+                      K.c_beta_adv * advv[V_BETA + i];
+    rhs[V_B + i] = K.S_B * (rhs[V_XT + i] - K.eta * Bv[i]) + K.c_beta_adv * (advv[V_B + i] - advv[V_XT + i]);
+  }
+}
+
+BssnK make_k(const StageLaunch& a, const double* prm) {
+  BssnK K;
+  for (int d = 0; d < 3; ++d) {
+    K.i12h[d] = 1.0 / (12.0 * a.h[d]);
+    K.i12h2[d] = 1.0 / (12.0 * a.h[d] * a.h[d]);
+    K.i24h[d] = 1.0 / (24.0 * a.h[d]);
+  }
+  K.i144hh[0] = 1.0 / (144.0 * a.h[0] * a.h[1]);
+  K.i144hh[1] = 1.0 / (144.0 * a.h[0] * a.h[2]);
+  K.i144hh[2] = 1.0 / (144.0 * a.h[1] * a.h[2]);
+  K.dt = a.dt; K.dt2 = a.dt / 2.0; K.dt3 = a.dt / 3.0; K.dt6 = a.dt / 6.0; K.third = 1.0 / 3.0;
+  K.F_alpha = prm[0]; K.n_alpha = prm[1]; K.L = prm[2]; K.eta_alpha = prm[3]; K.c_alpha_adv = prm[4];
+  K.C_beta = prm[5]; K.p_beta = prm[6]; K.S_B = prm[7]; K.eta = prm[8]; K.c_beta_adv = prm[9];
+  return K;
+}
+
+// One thread per interior point (x fastest).  STAGE 0 = RHS only (writes k to dst).
+template <int STAGE>
+__global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, double* rhs_dst) {
+  const Layout& L = a.L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = a.k_begin + blockIdx.z;
+  if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
+  const int64_t c = L.idx(i, j, k);
+  const int64_t gfs = L.gfs;
+  const double* in = (STAGE <= 1) ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b));
+  Strides st;
+  st.s[0] = 1; st.s[1] = L.px; st.s[2] = L.plane;
+  double r[NV];
+  bssn_point(in, gfs, c, st, K, r);
+  if (STAGE == 0) {
+    const int64_t ni = L.nx * L.ny * L.nz;
+    const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) rhs_dst[v * ni + o] = r[v];
+    return;
+  }
+  double* out = STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y));
+  const FaceDst fd = a.img[STAGE - 1];
+  const bool nf = near_face(L, i, j, k);
+  const unsigned long long code0 = a.step * (unsigned long long)NV;
+#pragma unroll 1
+  for (int v = 0; v < NV; ++v) {
+    const int64_t o = v * gfs + c;
+    double val;
+    if (STAGE == 1) val = fma(K.dt2, r[v], ld(in + o));
+    if (STAGE == 2) {
+      const double yv = a.s.y[o], sv = ld(in + o);
+      a.s.q[o] = fma(K.dt3, r[v], (yv + sv) * K.third);
+      val = fma(K.dt2, r[v], yv);
+    }
+    if (STAGE == 3) val = fma(K.dt, r[v], a.s.y[o]);
+    if (STAGE == 4) val = fma(K.dt6, r[v], fma(ld(in + o), K.third, a.s.q[o]));
+    out[o] = val;
+    if (nf) store_images(out + v * gfs, fd.lo + v * gfs, fd.hi + v * gfs, L, i, j, k, val);
+    if (STAGE == 4) check_finite(a.nan_flag, code0 + v, val);
+  }
+}
+
+template <int STAGE>
+cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  dim3 block(32, 4, 1);
+  dim3 grid((unsigned)((a.L.nx + 31) / 32), (unsigned)((a.L.ny + 3) / 4), (unsigned)nk);
+  bssn_simple<STAGE><<<grid, block, 0, st>>>(a, K, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch(const StageLaunch& a, int stage, double* dst, cudaStream_t st, const double* hparams) {
+  const BssnK K = make_k(a, hparams);
+  switch (stage) {
+    case 0: return launch<0>(a, K, dst, st);
+    case 1: return launch<1>(a, K, dst, st);
+    case 2: return launch<2>(a, K, dst, st);
+    case 3: return launch<3>(a, K, dst, st);
+    case 4: return launch<4>(a, K, dst, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st) {
+  return dispatch(a, stage, nullptr, st, a.hparams);
+}
+cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st) {
+  return dispatch(a, 0, dst, st, a.hparams);
+}
+
 }  // namespace chemora

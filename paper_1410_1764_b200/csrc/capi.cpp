@@ -230,6 +230,7 @@ StageLaunch stage_args(chemora_grid_t g, double dt) {
   a.dt = dt;
   a.fd_order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
   a.params = g->dparams;
+  for (int i = 0; i < kParams; ++i) a.hparams[i] = g->params[i];
   a.nan_flag = g->nan_flag;
   a.step = g->step;
   a.k_begin = 0;

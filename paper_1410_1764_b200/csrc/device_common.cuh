@@ -13,7 +13,7 @@ namespace chemora {
 // corners equal the doubly/triply wrapped interior value, exactly as the axis-by-axis fill.
 // Out of line: only threads near a face call it, and keeping its index arithmetic out of
 // the stage kernels' register allocation is worth the call.
-__device__ __noinline__ void store_images_n(double* own, double* zlo, double* zhi, int nx, int ny,
+static __device__ __noinline__ void store_images_n(double* own, double* zlo, double* zhi, int nx, int ny,
                                             int nz, int g, int64_t px, int64_t plane, int i, int j,
                                             int k, double v) {
   const int xi = i < g ? i + nx : (i >= nx - g ? i - nx : i);

@@ -31,6 +31,7 @@ struct StageLaunch {
   double dt;
   int fd_order;          // wave: 2/4/6/8
   const double* params;  // device copy of BSSN gauge params (10)
+  double hparams[10];    // host copy (folded into kernel arguments)
   unsigned long long* nan_flag;
   uint64_t step;         // global step index (for the non-finite report)
   int k_begin, k_end;    // local z-plane range [k_begin, k_end)

@@ -1,0 +1,165 @@
+"""GPU parity tests of the BSSN path: CUDA kernels behind the C ABI vs the CPU oracle on
+identical seeded inputs.  Tolerance (north_star): max relative error <= 1e-10 after 10 RK4
+steps, per GF normwise (max|gpu - oracle| / max|oracle|, reading R11)."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import chemora_inputs as ci
+import oracle
+
+pytestmark = pytest.mark.gpu
+B = 2
+BENCH = [2.0, 1.0, 1.0, 0.0, 1.0, 0.75, 0.0, 1.0, 1.0, 1.0]
+HARMONIC = [1.0, 2.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 1.0]
+
+
+def _mods():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1410_1764_b200 as P
+    from paper_1410_1764_b200 import capi as C
+    return P, C
+
+
+def relerr(a, b, floor=0.0):
+    out = []
+    for f in range(a.shape[0]):
+        s = max(np.abs(b[f]).max(), floor)
+        d = np.abs(a[f] - b[f]).max()
+        out.append(d / s if s > 0 else d)
+    return max(out)
+
+
+def perturbed(n, eps=1e-3, seed=1410):
+    h = tuple(1.0 / v for v in n)
+    return ci.mink_pert(n, h, seed, eps=eps), h
+
+
+@pytest.mark.parametrize("n", [(32, 32, 32), (36, 28, 44)])
+def test_rhs_parity_mink_pert(n):
+    P, C = _mods()
+    y0, h = perturbed(n, eps=1e-2)
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_initial(C.INIT_HOST, y0)
+    k = g.rhs().cpu().numpy()
+    ref = oracle.rhs(B, y0, h, BENCH)
+    assert relerr(k, ref) <= 1e-10
+
+
+def test_rhs_parity_pure_gauge():
+    """Strongly non-trivial data (the pure-gauge exact solution, App. A.4)."""
+    P, C = _mods()
+    from tests import bssn_exact
+    N = 24
+    n = (N, N, N)
+    h = (2 * math.pi / N,) * 3
+    z, y, x = ci.coords(n, h)
+    x, y, z = np.broadcast_arrays(x, y, z)
+    v = bssn_exact.bssn_vars(0.4, x, y, z)
+    state = np.zeros((25,) + x.shape)
+    for nm, arr in v.items():
+        state[ci.BSSN_GF.index(nm)] = arr
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_initial(C.INIT_HOST, state)
+    k = g.rhs().cpu().numpy()
+    ref = oracle.rhs(B, state, h, BENCH)
+    assert relerr(k, ref, floor=1e-3) <= 1e-11
+
+
+@pytest.mark.parametrize("params", [BENCH, HARMONIC])
+def test_rhs_parity_gauge_params(params):
+    P, C = _mods()
+    n = (20, 16, 24)
+    y0, h = perturbed(n, eps=2e-2, seed=3)
+    y0[ci.BSSN_GF.index("alpha")] += 0.1
+    g = P.Grid(C.SYS_BSSN, n, h, params=params)
+    g.set_initial(C.INIT_HOST, y0)
+    k = g.rhs().cpu().numpy()
+    ref = oracle.rhs(B, y0, h, params)
+    assert relerr(k, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [(32, 32, 32), (48, 48, 48), (36, 28, 44)])
+def test_rk4_parity_10_steps(n):
+    P, C = _mods()
+    y0, h = perturbed(n)
+    dt = 0.25 * min(h)
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_initial(C.INIT_HOST, y0)
+    g.rk4_step(dt, 10)
+    got = g.get_state()
+    ref = oracle.rk4(B, y0, h, dt, 10, BENCH)
+    # compare the change from the initial data too (the perturbation is ~1e-3 of flat)
+    assert relerr(got, ref) <= 1e-10
+    assert relerr(got - y0, ref - y0) <= 1e-8
+
+
+def test_gauge_wave_parity():
+    P, C = _mods()
+    n = (64, 6, 6)
+    h = (1.0 / 64, 1.0 / 6, 1.0 / 6)
+    y0 = ci.gauge_wave(n, h, shift=0.5)
+    g = P.Grid(C.SYS_BSSN, n, h, params=HARMONIC)
+    g.set_initial(C.INIT_HOST, y0)
+    dt = 0.25 / 64
+    g.rk4_step(dt, 10)
+    ref = oracle.rk4(B, y0, h, dt, 10, HARMONIC)
+    assert relerr(g.get_state(), ref) <= 1e-10
+
+
+def test_device_mink_pert_matches_inputs_module():
+    P, C = _mods()
+    n = (24, 20, 16)
+    h = tuple(1.0 / v for v in n)
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_initial(C.INIT_MINK_PERT, kind_params=[1e-3], seed=1410)
+    np.testing.assert_allclose(g.get_state(), ci.mink_pert(n, h, 1410, eps=1e-3), rtol=0, atol=1e-15)
+
+
+def test_local_slabs_bitwise_bssn():
+    P, C = _mods()
+    n = (16, 12, 24)
+    y0, h = perturbed(n)
+    dt = 0.25 * min(h)
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_initial(C.INIT_HOST, y0)
+    g.rk4_step(dt, 3)
+    s = P.LocalSlabs(C.SYS_BSSN, n, h, 2)
+    s.set_initial(C.INIT_HOST, y0)
+    s.rk4_step(dt, 3)
+    assert np.array_equal(s.get_state(), g.get_state())
+
+
+def test_full_size_192_sampled_parity():
+    """Benchmark configuration (192^3, MINK_PERT, benchmark gauge): one RK4 step, then
+    sampled points vs the oracle run on a (2R+1)^3 periodic box around each point
+    (wrap errors travel 3 points per stage, so R = 13 leaves the centre exact)."""
+    P, C = _mods()
+    N = 192
+    n = (N, N, N)
+    h = (1.0 / N,) * 3
+    dt = 0.25 * h[0]
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_initial(C.INIT_MINK_PERT, kind_params=[1e-3], seed=1410)
+    y0 = g.get_state()
+    g.rk4_step(dt, 1)
+    state = g.get_state()
+    R = 13
+    pts = [(0, 0, 0), (191, 191, 191), (5, 190, 100), (100, 50, 3)]
+    rng = np.random.default_rng(1)
+    pts += [tuple(int(v) for v in rng.integers(0, N, 3)) for _ in range(4)]
+    for (i, j, k) in pts:
+        lo = (i - R, j - R, k - R)
+        box = ci.mink_pert((2 * R + 1,) * 3, h, 1410, eps=1e-3,
+                           origin=tuple(l * hh for l, hh in zip(lo, h)), length=1.0)
+        ref = oracle.rk4(B, box, h, dt, 1, BENCH)[:, R, R, R]
+        got = state[:, k, j, i]
+        d0 = box[:, R, R, R]
+        # the device init matches the box generator to roundoff
+        np.testing.assert_allclose(y0[:, k, j, i], d0, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(got - d0, ref - d0, rtol=1e-8, atol=1e-13)
