@@ -82,10 +82,24 @@ __device__ __forceinline__ double adv(const double* __restrict__ f, int64_t c, c
   return r;
 }
 
-// Evaluate the 25 right-hand sides at interior offset c of the input set `in`.
-// (Advection terms included.)  App. A.2-A.3.
+// Output groups of the kernel fission (fission is "the most
+// important performance optimization" for the Einstein equations).
+// G0 = everything in one kernel; G1 = phi, gt, alpha, beta (kinematics, first
+// derivatives only); G2 = trK, At, A (curvature: Ricci, D_i D_j alpha); G3 = Xt, B
+// (second derivatives of the shift).
+__host__ __device__ constexpr bool in_group(int G, int v) {
+  return G == 0 ? true
+       : G == 1 ? (v == V_PHI || (v >= V_GT && v < V_GT + 6) || v == V_ALPHA || (v >= V_BETA && v < V_BETA + 3))
+       : G == 2 ? (v == V_TRK || (v >= V_AT && v < V_AT + 6) || v == V_AUX)
+                : ((v >= V_XT && v < V_XT + 3) || (v >= V_B && v < V_B + 3));
+}
+
+// Evaluate the right-hand sides of group G at interior offset c of the input set `in`
+// (advection included); rhs[v] is written for every v in the group.  App. A.2-A.3.
+template <int G>
 __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_t gfs, int64_t c,
                                            const Strides& st, const BssnK& K, double* rhs) {
+  constexpr bool g1 = G == 0 || G == 1, g2 = G == 0 || G == 2, g3 = G == 0 || G == 3;
   auto F = [&](int v) { return in + v * gfs; };
   // ---- point values
   double gt[6], At[6];
@@ -98,256 +112,284 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
   for (int i = 0; i < 3; ++i) {
     Xt[i] = ld(F(V_XT + i) + c); beta[i] = ld(F(V_BETA + i) + c); Bv[i] = ld(F(V_B + i) + c);
   }
-  // ---- inverse conformal metric gu = adj(gt) / det(gt)
-  const double c00 = gt[3] * gt[5] - gt[4] * gt[4];
-  const double c01 = gt[2] * gt[4] - gt[1] * gt[5];
-  const double c02 = gt[1] * gt[4] - gt[2] * gt[3];
-  const double det = gt[0] * c00 + gt[1] * c01 + gt[2] * c02;
-  const double idet = 1.0 / det;
-  double gu[6];
-  gu[0] = c00 * idet;
-  gu[1] = c01 * idet;
-  gu[2] = c02 * idet;
-  gu[3] = (gt[0] * gt[5] - gt[2] * gt[2]) * idet;
-  gu[4] = (gt[1] * gt[2] - gt[0] * gt[4]) * idet;
-  gu[5] = (gt[0] * gt[3] - gt[1] * gt[1]) * idet;
-  const double em4phi = exp(-4.0 * phi);
+  double dbeta[3][3];  // dbeta[l][k] = d_l beta^k
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dbeta[l][k] = D1raw(F(V_BETA + k), c, st.s[l]) * K.i12h[l];
+  const double divb = dbeta[0][0] + dbeta[1][1] + dbeta[2][2];
 
-  // ---- first derivatives of the metric -> Christoffels (first kind Gl, second kind Gu)
-  double Gl[3][6];  // Gl[i][s(j,k)] = 1/2 (d_j gt_ik + d_k gt_ij - d_i gt_jk)
-  {
-    double dg[3][6];
+  if (g1) {
+    rhs[V_PHI] = (divb - alpha * trK) * (1.0 / 6.0);
 #pragma unroll
-    for (int l = 0; l < 3; ++l)
+    for (int s = 0; s < 6; ++s) {
+      const int i = sI(s), j = sJ(s);
+      double rg = -2.0 * alpha * At[s] - (2.0 / 3.0) * gt[s] * divb;
 #pragma unroll
-      for (int s = 0; s < 6; ++s) dg[l][s] = D1raw(F(V_GT + s), c, st.s[l]) * K.i12h[l];
+      for (int k = 0; k < 3; ++k) {
+        rg = fma(gt[sy(i, k)], dbeta[j][k], rg);
+        rg = fma(gt[sy(j, k)], dbeta[i][k], rg);
+      }
+      rhs[V_GT + s] = rg;
+    }
+    const double apow_n = (K.n_alpha == 1.0) ? alpha : pow(alpha, K.n_alpha);
+    rhs[V_ALPHA] = -K.F_alpha * apow_n * (K.L * Aux + (1.0 - K.L) * trK);
+    const double apow_p = (K.p_beta == 0.0) ? 1.0 : pow(alpha, K.p_beta);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      rhs[V_BETA + i] = K.C_beta * apow_p * (K.S_B * Bv[i] + (1.0 - K.S_B) * (Xt[i] - K.eta * beta[i]));
+  }
+
+  if (g2 || g3) {
+    // ---- inverse conformal metric gu = adj(gt) / det(gt)
+    const double c00 = gt[3] * gt[5] - gt[4] * gt[4];
+    const double c01 = gt[2] * gt[4] - gt[1] * gt[5];
+    const double c02 = gt[1] * gt[4] - gt[2] * gt[3];
+    const double det = gt[0] * c00 + gt[1] * c01 + gt[2] * c02;
+    const double idet = 1.0 / det;
+    double gu[6];
+    gu[0] = c00 * idet;
+    gu[1] = c01 * idet;
+    gu[2] = c02 * idet;
+    gu[3] = (gt[0] * gt[5] - gt[2] * gt[2]) * idet;
+    gu[4] = (gt[1] * gt[2] - gt[0] * gt[4]) * idet;
+    gu[5] = (gt[0] * gt[3] - gt[1] * gt[1]) * idet;
+
+    // ---- first derivatives of the metric -> Christoffels (first kind Gl, second kind Gu)
+    double Gl[3][6];  // Gl[i][s(j,k)] = 1/2 (d_j gt_ik + d_k gt_ij - d_i gt_jk)
+    {
+      double dg[3][6];
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int s = 0; s < 6; ++s) dg[l][s] = D1raw(F(V_GT + s), c, st.s[l]) * K.i12h[l];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+          const int j = sI(s), k = sJ(s);
+          Gl[i][s] = 0.5 * (dg[j][sy(i, k)] + dg[k][sy(i, j)] - dg[i][s]);
+        }
+    }
+    double Gu[3][6];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int j = sI(s), k = sJ(s);
-        Gl[i][s] = 0.5 * (dg[j][sy(i, k)] + dg[k][sy(i, j)] - dg[i][s]);
-      }
-  }
-  double Gu[3][6];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int s = 0; s < 6; ++s)
-      Gu[i][s] = gu[sy(i, 0)] * Gl[0][s] + gu[sy(i, 1)] * Gl[1][s] + gu[sy(i, 2)] * Gl[2][s];
-  double Xtn[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    double a = 0.0;
-#pragma unroll
-    for (int s = 0; s < 6; ++s) a = fma(mult(s) * gu[s], Gu[i][s], a);
-    Xtn[i] = a;
-  }
-  // ---- other first derivatives
-  double dphi[3], dalpha[3], dtrK[3], dbeta[3][3], dXt[3][3];  // dbeta[l][k] = d_l beta^k
-#pragma unroll
-  for (int l = 0; l < 3; ++l) {
-    dphi[l] = D1raw(F(V_PHI), c, st.s[l]) * K.i12h[l];
-    dalpha[l] = D1raw(F(V_ALPHA), c, st.s[l]) * K.i12h[l];
-    dtrK[l] = D1raw(F(V_TRK), c, st.s[l]) * K.i12h[l];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      dbeta[l][k] = D1raw(F(V_BETA + k), c, st.s[l]) * K.i12h[l];
-      dXt[l][k] = D1raw(F(V_XT + k), c, st.s[l]) * K.i12h[l];
-    }
-  }
-  // ---- conformal Ricci tensor R~_ij
-  double Rt[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) Rt[s] = 0.0;
-  // -1/2 gu^lm d_l d_m gt_ij, pair (l,m) at a time
-#pragma unroll
-  for (int p = 0; p < 6; ++p) {
-    const int l = sI(p), m = sJ(p);
-    const double w = -0.5 * mult(p) * gu[p];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const double* f = F(V_GT + s);
-      const double dd = (l == m) ? D2raw(f, c, st.s[l], gt[s]) * K.i12h2[l]
-                                 : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
-      Rt[s] = fma(w, dd, Rt[s]);
-    }
-  }
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    const int i = sI(s), j = sJ(s);
-    double r = Rt[s];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      r = fma(0.5 * gt[sy(k, i)], dXt[j][k], r);
-      r = fma(0.5 * gt[sy(k, j)], dXt[i][k], r);
-      r = fma(0.5 * Xtn[k], Gl[i][sy(j, k)] + Gl[j][sy(i, k)], r);
-    }
-#pragma unroll
-    for (int l = 0; l < 3; ++l)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        double t = 0.0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          t = fma(Gu[k][sy(l, i)], Gl[j][sy(k, m)], t);
-          t = fma(Gu[k][sy(l, j)], Gl[i][sy(k, m)], t);
-          t = fma(Gu[k][sy(i, m)], Gl[k][sy(l, j)], t);
-        }
-        r = fma(gu[sy(l, m)], t, r);
-      }
-    Rt[s] = r;
-  }
-  // ---- phi terms: D~_i D~_j phi, traces
-  double DDphi[6], DDalpha[6];
-  double ddalpha[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    const int i = sI(s), j = sJ(s);
-    const double ddp = (i == j) ? D2raw(F(V_PHI), c, st.s[i], phi) * K.i12h2[i]
-                                : D11raw(F(V_PHI), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
-    const double dda = (i == j) ? D2raw(F(V_ALPHA), c, st.s[i], alpha) * K.i12h2[i]
-                                : D11raw(F(V_ALPHA), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
-    ddalpha[s] = dda;
-    DDphi[s] = ddp - (Gu[0][s] * dphi[0] + Gu[1][s] * dphi[1] + Gu[2][s] * dphi[2]);
-  }
-  double gudphi[3];  // gt^kl d_l phi
-#pragma unroll
-  for (int k = 0; k < 3; ++k) gudphi[k] = gu[sy(k, 0)] * dphi[0] + gu[sy(k, 1)] * dphi[1] + gu[sy(k, 2)] * dphi[2];
-  double trDDphi = 0.0, dphi2 = 0.0;
-#pragma unroll
-  for (int s = 0; s < 6; ++s) trDDphi = fma(mult(s) * gu[s], DDphi[s], trDDphi);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) dphi2 = fma(gudphi[k], dphi[k], dphi2);
-  // D_i D_j alpha with the physical Christoffel
-  // Gamma^k_ij = Gu^k_ij + 2 (delta^k_i d_j phi + delta^k_j d_i phi - gt_ij gt^kl d_l phi)
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    const int i = sI(s), j = sJ(s);
-    double gam_da = Gu[0][s] * dalpha[0] + Gu[1][s] * dalpha[1] + Gu[2][s] * dalpha[2];
-    const double gdpda = gudphi[0] * dalpha[0] + gudphi[1] * dalpha[1] + gudphi[2] * dalpha[2];
-    gam_da += 2.0 * (dalpha[i] * dphi[j] + dalpha[j] * dphi[i] - gt[s] * gdpda);
-    DDalpha[s] = ddalpha[s] - gam_da;
-  }
-  double trDDalpha;
-  {
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int s = 0; s < 6; ++s) s1 = fma(mult(s) * gu[s], ddalpha[s], s1);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { s2 = fma(Xtn[k], dalpha[k], s2); s3 = fma(gudphi[k], dalpha[k], s3); }
-    trDDalpha = em4phi * (s1 - s2 + 2.0 * s3);
-  }
-  // ---- R_ij = R~_ij + R^phi_ij ; X_ij = -D_i D_j alpha + alpha R_ij
-  double X[6], trX = 0.0;
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    const int i = sI(s), j = sJ(s);
-    const double Rphi = -2.0 * DDphi[s] - 2.0 * gt[s] * trDDphi + 4.0 * dphi[i] * dphi[j] - 4.0 * gt[s] * dphi2;
-    X[s] = fma(alpha, Rt[s] + Rphi, -DDalpha[s]);
-    trX = fma(mult(s) * gu[s], X[s], trX);
-  }
-  // ---- raised At: Am[i][j] = At^i_j (full 3x3), Au = At^ij (sym)
-  double Am[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      Am[i][j] = gu[sy(i, 0)] * At[sy(0, j)] + gu[sy(i, 1)] * At[sy(1, j)] + gu[sy(i, 2)] * At[sy(2, j)];
-  double Au[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    const int i = sI(s), j = sJ(s);
-    Au[s] = Am[i][0] * gu[sy(0, j)] + Am[i][1] * gu[sy(1, j)] + Am[i][2] * gu[sy(2, j)];
-  }
-  double AA = 0.0;
-#pragma unroll
-  for (int s = 0; s < 6; ++s) AA = fma(mult(s) * At[s], Au[s], AA);
-  const double divb = dbeta[0][0] + dbeta[1][1] + dbeta[2][2];
-
-  // ---- RHS (without advection; added below)
-  rhs[V_PHI] = (divb - alpha * trK) * (1.0 / 6.0);
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    const int i = sI(s), j = sJ(s);
-    double rg = -2.0 * alpha * At[s] - (2.0 / 3.0) * gt[s] * divb;
-    double ra = em4phi * (X[s] - (1.0 / 3.0) * gt[s] * trX) - (2.0 / 3.0) * At[s] * divb;
-    double aam = 0.0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      rg = fma(gt[sy(i, k)], dbeta[j][k], rg);
-      rg = fma(gt[sy(j, k)], dbeta[i][k], rg);
-      ra = fma(At[sy(i, k)], dbeta[j][k], ra);
-      ra = fma(At[sy(j, k)], dbeta[i][k], ra);
-      aam = fma(At[sy(i, k)], Am[k][j], aam);
-    }
-    ra = fma(alpha, trK * At[s] - 2.0 * aam, ra);
-    rhs[V_GT + s] = rg;
-    rhs[V_AT + s] = ra;
-  }
-  const double rhs_trK_noadv = -trDDalpha + alpha * (AA + trK * trK * (1.0 / 3.0));
-  rhs[V_TRK] = rhs_trK_noadv;
-  // Xt: needs second derivatives of beta
-  double ddivb[3] = {0.0, 0.0, 0.0};  // d_j (d . beta)
-  double lapb[3] = {0.0, 0.0, 0.0};   // gt^jk d_j d_k beta^i
-#pragma unroll
-  for (int p = 0; p < 6; ++p) {
-    const int l = sI(p), m = sJ(p);
+      for (int s = 0; s < 6; ++s)
+        Gu[i][s] = gu[sy(i, 0)] * Gl[0][s] + gu[sy(i, 1)] * Gl[1][s] + gu[sy(i, 2)] * Gl[2][s];
+    double Xtn[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double* f = F(V_BETA + i);
-      const double dd = (l == m) ? D2raw(f, c, st.s[l], beta[i]) * K.i12h2[l]
-                                 : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
-      lapb[i] = fma(mult(p) * gu[p], dd, lapb[i]);
-      // d_l d_m beta^i contributes to d_j(d.beta) for (j = l, i = m) and (j = m, i = l)
-      if (i == m) ddivb[l] += dd;
-      if (i == l && l != m) ddivb[m] += dd;
+      double a = 0.0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) a = fma(mult(s) * gu[s], Gu[i][s], a);
+      Xtn[i] = a;
+    }
+    double dphi[3], dalpha[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      dphi[l] = D1raw(F(V_PHI), c, st.s[l]) * K.i12h[l];
+      dalpha[l] = D1raw(F(V_ALPHA), c, st.s[l]) * K.i12h[l];
+    }
+    // ---- raised At: Am[i][j] = At^i_j (full 3x3), Au = At^ij (sym)
+    double Am[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        Am[i][j] = gu[sy(i, 0)] * At[sy(0, j)] + gu[sy(i, 1)] * At[sy(1, j)] + gu[sy(i, 2)] * At[sy(2, j)];
+    double Au[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int i = sI(s), j = sJ(s);
+      Au[s] = Am[i][0] * gu[sy(0, j)] + Am[i][1] * gu[sy(1, j)] + Am[i][2] * gu[sy(2, j)];
+    }
+
+    if (g2) {
+      const double em4phi = exp(-4.0 * phi);
+      double dXt[3][3];  // dXt[l][k] = d_l Xt^k
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dXt[l][k] = D1raw(F(V_XT + k), c, st.s[l]) * K.i12h[l];
+      // ---- conformal Ricci tensor R~_ij
+      double Rt[6];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) Rt[s] = 0.0;
+      // -1/2 gu^lm d_l d_m gt_ij, pair (l,m) at a time
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const int l = sI(p), m = sJ(p);
+        const double w = -0.5 * mult(p) * gu[p];
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+          const double* f = F(V_GT + s);
+          const double dd = (l == m) ? D2raw(f, c, st.s[l], gt[s]) * K.i12h2[l]
+                                     : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
+          Rt[s] = fma(w, dd, Rt[s]);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int i = sI(s), j = sJ(s);
+        double r = Rt[s];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          r = fma(0.5 * gt[sy(k, i)], dXt[j][k], r);
+          r = fma(0.5 * gt[sy(k, j)], dXt[i][k], r);
+          r = fma(0.5 * Xtn[k], Gl[i][sy(j, k)] + Gl[j][sy(i, k)], r);
+        }
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              t = fma(Gu[k][sy(l, i)], Gl[j][sy(k, m)], t);
+              t = fma(Gu[k][sy(l, j)], Gl[i][sy(k, m)], t);
+              t = fma(Gu[k][sy(i, m)], Gl[k][sy(l, j)], t);
+            }
+            r = fma(gu[sy(l, m)], t, r);
+          }
+        Rt[s] = r;
+      }
+      // ---- phi terms: D~_i D~_j phi, traces; second derivatives of alpha
+      double DDphi[6], DDalpha[6], ddalpha[6];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int i = sI(s), j = sJ(s);
+        const double ddp = (i == j) ? D2raw(F(V_PHI), c, st.s[i], phi) * K.i12h2[i]
+                                    : D11raw(F(V_PHI), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
+        const double dda = (i == j) ? D2raw(F(V_ALPHA), c, st.s[i], alpha) * K.i12h2[i]
+                                    : D11raw(F(V_ALPHA), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
+        ddalpha[s] = dda;
+        DDphi[s] = ddp - (Gu[0][s] * dphi[0] + Gu[1][s] * dphi[1] + Gu[2][s] * dphi[2]);
+      }
+      double gudphi[3];  // gt^kl d_l phi
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gudphi[k] = gu[sy(k, 0)] * dphi[0] + gu[sy(k, 1)] * dphi[1] + gu[sy(k, 2)] * dphi[2];
+      double trDDphi = 0.0, dphi2 = 0.0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) trDDphi = fma(mult(s) * gu[s], DDphi[s], trDDphi);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dphi2 = fma(gudphi[k], dphi[k], dphi2);
+      // D_i D_j alpha with Gamma^k_ij = Gu^k_ij + 2 (delta^k_i d_j phi + delta^k_j d_i phi
+      //                                             - gt_ij gt^kl d_l phi)
+      const double gdpda = gudphi[0] * dalpha[0] + gudphi[1] * dalpha[1] + gudphi[2] * dalpha[2];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int i = sI(s), j = sJ(s);
+        double gam_da = Gu[0][s] * dalpha[0] + Gu[1][s] * dalpha[1] + Gu[2][s] * dalpha[2];
+        gam_da += 2.0 * (dalpha[i] * dphi[j] + dalpha[j] * dphi[i] - gt[s] * gdpda);
+        DDalpha[s] = ddalpha[s] - gam_da;
+      }
+      double trDDalpha;
+      {
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) s1 = fma(mult(s) * gu[s], ddalpha[s], s1);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s2 = fma(Xtn[k], dalpha[k], s2);
+        trDDalpha = em4phi * (s1 - s2 + 2.0 * gdpda);
+      }
+      // ---- X_ij = -D_i D_j alpha + alpha (R~_ij + R^phi_ij)
+      double X[6], trX = 0.0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int i = sI(s), j = sJ(s);
+        const double Rphi = -2.0 * DDphi[s] - 2.0 * gt[s] * trDDphi + 4.0 * dphi[i] * dphi[j] - 4.0 * gt[s] * dphi2;
+        X[s] = fma(alpha, Rt[s] + Rphi, -DDalpha[s]);
+        trX = fma(mult(s) * gu[s], X[s], trX);
+      }
+      double AA = 0.0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) AA = fma(mult(s) * At[s], Au[s], AA);
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int i = sI(s), j = sJ(s);
+        double ra = em4phi * (X[s] - (1.0 / 3.0) * gt[s] * trX) - (2.0 / 3.0) * At[s] * divb;
+        double aam = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          ra = fma(At[sy(i, k)], dbeta[j][k], ra);
+          ra = fma(At[sy(j, k)], dbeta[i][k], ra);
+          aam = fma(At[sy(i, k)], Am[k][j], aam);
+        }
+        rhs[V_AT + s] = fma(alpha, trK * At[s] - 2.0 * aam, ra);
+      }
+      rhs[V_TRK] = -trDDalpha + alpha * (AA + trK * trK * (1.0 / 3.0));
+    }
+
+    if (g3) {
+      double dtrK[3];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) dtrK[l] = D1raw(F(V_TRK), c, st.s[l]) * K.i12h[l];
+      double ddivb[3] = {0.0, 0.0, 0.0};  // d_j (d . beta)
+      double lapb[3] = {0.0, 0.0, 0.0};   // gt^jk d_j d_k beta^i
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const int l = sI(p), m = sJ(p);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double* f = F(V_BETA + i);
+          const double dd = (l == m) ? D2raw(f, c, st.s[l], beta[i]) * K.i12h2[l]
+                                     : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
+          lapb[i] = fma(mult(p) * gu[p], dd, lapb[i]);
+          // d_l d_m beta^i feeds d_j (d.beta) for (j = l, i = m) and (j = m, i = l)
+          if (i == m) ddivb[l] += dd;
+          if (i == l && l != m) ddivb[m] += dd;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double r = lapb[i] + (1.0 / 3.0) * (gu[sy(i, 0)] * ddivb[0] + gu[sy(i, 1)] * ddivb[1] + gu[sy(i, 2)] * ddivb[2]);
+        r = fma((2.0 / 3.0) * Xtn[i], divb, r);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          r = fma(-Xtn[j], dbeta[j][i], r);
+          r = fma(-2.0 * Au[sy(i, j)], dalpha[j], r);
+          s = fma(6.0 * Au[sy(i, j)], dphi[j], s);
+          s = fma(-(2.0 / 3.0) * gu[sy(i, j)], dtrK[j], s);
+        }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) s = fma(mult(q) * Gu[i][q], Au[q], s);
+        rhs[V_XT + i] = fma(2.0 * alpha, s, r);
+      }
     }
   }
+
+  // ---- advection (App. A.2 Adv) and the gauge couplings that need the full RHS
+  auto centre = [&](int v) -> double {
+    if (v == V_PHI) return phi;
+    if (v >= V_GT && v < V_GT + 6) return gt[v - V_GT];
+    if (v == V_TRK) return trK;
+    if (v >= V_AT && v < V_AT + 6) return At[v - V_AT];
+    if (v >= V_XT && v < V_XT + 3) return Xt[v - V_XT];
+    if (v == V_ALPHA) return alpha;
+    if (v == V_AUX) return Aux;
+    if (v >= V_BETA && v < V_BETA + 3) return beta[v - V_BETA];
+    return Bv[v - V_B];
+  };
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    double r = lapb[i] + (1.0 / 3.0) * (gu[sy(i, 0)] * ddivb[0] + gu[sy(i, 1)] * ddivb[1] + gu[sy(i, 2)] * ddivb[2]);
-    r = fma((2.0 / 3.0) * Xtn[i], divb, r);
-    double s = 0.0;
+  for (int v = 0; v < V_ALPHA; ++v)
+    if (in_group(G, v)) rhs[v] += adv(F(v), c, st, beta, centre(v), K);
+  if (g1) {
+    rhs[V_ALPHA] = fma(K.c_alpha_adv, adv(F(V_ALPHA), c, st, beta, alpha, K), rhs[V_ALPHA]);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      r = fma(-Xtn[j], dbeta[j][i], r);
-      r = fma(-2.0 * Au[sy(i, j)], dalpha[j], r);
-      s = fma(6.0 * Au[sy(i, j)], dphi[j], s);
-      s = fma(-(2.0 / 3.0) * gu[sy(i, j)], dtrK[j], s);
+    for (int i = 0; i < 3; ++i)
+      rhs[V_BETA + i] = fma(K.c_beta_adv, adv(F(V_BETA + i), c, st, beta, beta[i], K), rhs[V_BETA + i]);
+  }
+  if (g2)
+    rhs[V_AUX] = K.L * (rhs[V_TRK] - K.eta_alpha * Aux) + K.c_alpha_adv * adv(F(V_AUX), c, st, beta, Aux, K);
+  if (g3) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double advB = adv(F(V_B + i), c, st, beta, Bv[i], K);
+      const double advX = adv(F(V_XT + i), c, st, beta, Xt[i], K);
+      rhs[V_B + i] = K.S_B * (rhs[V_XT + i] - K.eta * Bv[i]) + K.c_beta_adv * (advB - advX);
     }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) s = fma(mult(q) * Gu[i][q], Au[q], s);
-    rhs[V_XT + i] = fma(2.0 * alpha, s, r);
-  }
-  // ---- advection of every GF, and the gauge equations (App. A.3)
-  double advv[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double f0;
-    if (v == V_PHI) f0 = phi;
-    else if (v >= V_GT && v < V_GT + 6) f0 = gt[v - V_GT];
-    else if (v == V_TRK) f0 = trK;
-    else if (v >= V_AT && v < V_AT + 6) f0 = At[v - V_AT];
-    else if (v >= V_XT && v < V_XT + 3) f0 = Xt[v - V_XT];
-    else if (v == V_ALPHA) f0 = alpha;
-    else if (v == V_AUX) f0 = Aux;
-    else if (v >= V_BETA && v < V_BETA + 3) f0 = beta[v - V_BETA];
-    else f0 = Bv[v - V_B];
-    advv[v] = adv(F(v), c, st, beta, f0, K);
-  }
-#pragma unroll
-  for (int v = 0; v < V_ALPHA; ++v) rhs[v] += advv[v];
-  const double rhs_trK = rhs[V_TRK];
-  const double apow_n = (K.n_alpha == 1.0) ? alpha : pow(alpha, K.n_alpha);
-  rhs[V_ALPHA] = -K.F_alpha * apow_n * (K.L * Aux + (1.0 - K.L) * trK) + K.c_alpha_adv * advv[V_ALPHA];
-  rhs[V_AUX] = K.L * (rhs_trK - K.eta_alpha * Aux) + K.c_alpha_adv * advv[V_AUX];
-  const double apow_p = (K.p_beta == 0.0) ? 1.0 : pow(alpha, K.p_beta);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    rhs[V_BETA + i] = K.C_beta * apow_p * (K.S_B * Bv[i] + (1.0 - K.S_B) * (Xt[i] - K.eta * beta[i])) +
-                      K.c_beta_adv * advv[V_BETA + i];
-    rhs[V_B + i] = K.S_B * (rhs[V_XT + i] - K.eta * Bv[i]) + K.c_beta_adv * (advv[V_B + i] - advv[V_XT + i]);
   }
 }
 
@@ -367,8 +409,9 @@ BssnK make_k(const StageLaunch& a, const double* prm) {
   return K;
 }
 
-// One thread per interior point (x fastest).  STAGE 0 = RHS only (writes k to dst).
-template <int STAGE>
+// One thread per interior point (x fastest), computing the RHS group G and applying the
+// RK4 stage update to that group's GFs.  STAGE 0 = RHS only (writes k to dst).
+template <int STAGE, int G>
 __global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, double* rhs_dst) {
   const Layout& L = a.L;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -381,20 +424,22 @@ __global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, doubl
   Strides st;
   st.s[0] = 1; st.s[1] = L.px; st.s[2] = L.plane;
   double r[NV];
-  bssn_point(in, gfs, c, st, K, r);
+  bssn_point<G>(in, gfs, c, st, K, r);
   if (STAGE == 0) {
     const int64_t ni = L.nx * L.ny * L.nz;
     const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) rhs_dst[v * ni + o] = r[v];
+    for (int v = 0; v < NV; ++v)
+      if (in_group(G, v)) rhs_dst[v * ni + o] = r[v];
     return;
   }
   double* out = STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y));
   const FaceDst fd = a.img[STAGE - 1];
   const bool nf = near_face(L, i, j, k);
   const unsigned long long code0 = a.step * (unsigned long long)NV;
-#pragma unroll 1
+#pragma unroll
   for (int v = 0; v < NV; ++v) {
+    if (!in_group(G, v)) continue;
     const int64_t o = v * gfs + c;
     double val;
     if (STAGE == 1) val = fma(K.dt2, r[v], ld(in + o));
@@ -411,24 +456,34 @@ __global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, doubl
   }
 }
 
-template <int STAGE>
+template <int STAGE, int G>
 cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
   dim3 block(32, 4, 1);
   dim3 grid((unsigned)((a.L.nx + 31) / 32), (unsigned)((a.L.ny + 3) / 4), (unsigned)nk);
-  bssn_simple<STAGE><<<grid, block, 0, st>>>(a, K, dst);
+  bssn_simple<STAGE, G><<<grid, block, 0, st>>>(a, K, dst);
   return cudaGetLastError();
+}
+
+template <int STAGE>
+cudaError_t launch_stage(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
+  // variant 1: the fused single kernel; default: the fissioned kernels G1, G2, G3
+  if (a.variant == 1) return launch<STAGE, 0>(a, K, dst, st);
+  cudaError_t e = launch<STAGE, 1>(a, K, dst, st);
+  if (e == cudaSuccess) e = launch<STAGE, 2>(a, K, dst, st);
+  if (e == cudaSuccess) e = launch<STAGE, 3>(a, K, dst, st);
+  return e;
 }
 
 cudaError_t dispatch(const StageLaunch& a, int stage, double* dst, cudaStream_t st, const double* hparams) {
   const BssnK K = make_k(a, hparams);
   switch (stage) {
-    case 0: return launch<0>(a, K, dst, st);
-    case 1: return launch<1>(a, K, dst, st);
-    case 2: return launch<2>(a, K, dst, st);
-    case 3: return launch<3>(a, K, dst, st);
-    case 4: return launch<4>(a, K, dst, st);
+    case 0: return launch_stage<0>(a, K, dst, st);
+    case 1: return launch_stage<1>(a, K, dst, st);
+    case 2: return launch_stage<2>(a, K, dst, st);
+    case 3: return launch_stage<3>(a, K, dst, st);
+    case 4: return launch_stage<4>(a, K, dst, st);
   }
   return cudaErrorInvalidValue;
 }
