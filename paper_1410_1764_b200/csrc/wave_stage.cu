@@ -16,6 +16,7 @@
 #include "grid.hpp"
 #include "kernels.hpp"
 #include "device_common.cuh"
+#include "tma.cuh"
 
 namespace chemora {
 namespace {
@@ -253,6 +254,233 @@ cudaError_t launch_simple(const StageLaunch& a, const WaveK& K, double* dst, cud
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ TMA z-march kernel
+// The B200-native tiling: a CTA owns a TX x TY tile of the x-y plane and marches up a chunk
+// of z planes.  One elected producer thread streams the stencil operands into shared
+// memory with TMA (cp.async.bulk.tensor, 4-D maps over a state set [gf][z][y][x]):
+//   ring Z (depth 2W+3): per plane, rho with its x/y halo and v3 -- the two GFs that are
+//                        differentiated along z, so 2W+1 planes of them stay resident;
+//   ring P (depth 3):    per plane, v1 with its x halo and v2 with its y halo.
+// Eight consumer warps compute two points per thread per plane from shared memory (x/y/z
+// derivatives all from SMEM, no redundant HBM or L2 reads), load the pointwise operands
+// (y, Q) with coalesced loads, and store the stage outputs (+ ghost images).  Full/empty
+// mbarriers per slot; the producer runs up to 3 planes ahead.  Arithmetic is operation-for-
+// operation that of wave_simple (bitwise-identical results; this file has no FMA
+// contraction).
+template <int W>
+struct TmaCfg {
+  static constexpr int TX = 32, TY = 16;
+  static constexpr int RX = TX + 2 * W, RY = TY + 2 * W;
+  static constexpr int RZ = 2 * W + 3, RP = 3;
+  static constexpr int r128(int b) { return (b + 127) / 128 * 128; }
+  static constexpr int ZRHO_B = r128(RX * RY * 8), ZV3_B = r128(TX * TY * 8), ZSLOT = ZRHO_B + ZV3_B;
+  static constexpr int PV1_B = r128(RX * TY * 8), PV2_B = r128(TX * RY * 8), PSLOT = PV1_B + PV2_B;
+  static constexpr uint32_t ZBYTES = (RX * RY + TX * TY) * 8;
+  static constexpr uint32_t PBYTES = (RX * TY + TX * RY) * 8;
+  static constexpr int SMEM = RZ * ZSLOT + RP * PSLOT + (2 * RZ + 2 * RP) * 8;
+  static constexpr int NCW = 8;  // consumer warps
+};
+
+template <int W>
+__device__ __forceinline__ double d1s(const double* f, int c, int s) {
+  double acc = 0.0;
+#pragma unroll
+  for (int q = W; q >= 1; --q) acc = fma(D1W<W>::c(q), f[c + q * s] - f[c - q * s], acc);
+  return acc;
+}
+
+template <int STAGE, int W>
+__global__ void __launch_bounds__(288, 2)
+    wave_tma(const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmV1,
+             const __grid_constant__ CUtensorMap tmV2, const __grid_constant__ CUtensorMap tmC,
+             StageLaunch a, WaveK K, int kchunk) {
+  using Cf = TmaCfg<W>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* zbase = smem;
+  unsigned char* pbase = smem + Cf::RZ * Cf::ZSLOT;
+  uint64_t* zfull = reinterpret_cast<uint64_t*>(pbase + Cf::RP * Cf::PSLOT);
+  uint64_t* zempty = zfull + Cf::RZ;
+  uint64_t* pfull = zempty + Cf::RZ;
+  uint64_t* pempty = pfull + Cf::RP;
+  const Layout& L = a.L;
+  const int i0 = blockIdx.x * Cf::TX, j0 = blockIdx.y * Cf::TY;
+  const int kb = a.k_begin + blockIdx.z * kchunk;
+  const int ke = min(kb + kchunk, a.k_end);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cf::RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, Cf::NCW); }
+    for (int s = 0; s < Cf::RP; ++s) { mbar_init(pfull + s, 1); mbar_init(pempty + s, Cf::NCW); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (kb >= ke) return;
+  const int g = L.g;
+  const int nk = ke - kb;
+
+  if (warp == Cf::NCW) {  // ---------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&tmR); prefetch_tmap(&tmV1); prefetch_tmap(&tmV2); prefetch_tmap(&tmC);
+      auto loadZ = [&](int t) {  // plane kb - W + t
+        const int s = t % Cf::RZ, n = t / Cf::RZ;
+        if (n > 0) mbar_wait(zempty + s, (n - 1) & 1);
+        unsigned char* dst = zbase + s * Cf::ZSLOT;
+        const int zc = g + kb - W + t;
+        mbar_arrive_expect_tx(zfull + s, Cf::ZBYTES);
+        tma_load_4d(dst, &tmR, zfull + s, kXOff + i0 - W, g + j0 - W, zc, GRHO);
+        tma_load_4d(dst + Cf::ZRHO_B, &tmC, zfull + s, kXOff + i0, g + j0, zc, GV3);
+      };
+      auto loadP = [&](int t) {  // plane kb + t
+        const int s = t % Cf::RP, n = t / Cf::RP;
+        if (n > 0) mbar_wait(pempty + s, (n - 1) & 1);
+        unsigned char* dst = pbase + s * Cf::PSLOT;
+        const int zc = g + kb + t;
+        mbar_arrive_expect_tx(pfull + s, Cf::PBYTES);
+        tma_load_4d(dst, &tmV1, pfull + s, kXOff + i0 - W, g + j0, zc, GV1);
+        tma_load_4d(dst + Cf::PV1_B, &tmV2, pfull + s, kXOff + i0, g + j0 - W, zc, GV2);
+      };
+      for (int t = 0; t < 2 * W; ++t) loadZ(t);
+      for (int t = 0; t < nk; ++t) {
+        loadZ(t + 2 * W);
+        loadP(t);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: thread (lane, warp) owns points (lane, warp) and (lane, warp+8)
+  const int64_t gfs = L.gfs;
+  double* out = STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y));
+  const FaceDst fd = a.img[STAGE - 1];
+  const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
+  const int i = i0 + lane;
+  for (int t = 0; t < 2 * W; ++t) mbar_wait(zfull + t % Cf::RZ, (t / Cf::RZ) & 1);
+#pragma unroll 1
+  for (int t = 0; t < nk; ++t) {
+    const int k = kb + t;
+    // pointwise operands first so their latency overlaps the barrier wait
+    double Y[2][5], Qv[2][5], yu[2], qu[2];
+    int64_t cc[2];
+    bool live[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + warp + 8 * h;
+      live[h] = i < L.nx && j < L.ny;
+      cc[h] = L.idx(i, j, k);
+#pragma unroll
+      for (int f = 0; f < 5; ++f) { Y[h][f] = 0.0; Qv[h][f] = 0.0; }
+      yu[h] = 0.0; qu[h] = 0.0;
+      if (live[h]) {
+        if (STAGE == 2 || STAGE == 3) {
+#pragma unroll
+          for (int f = 1; f <= 4; ++f) Y[h][f] = a.s.y[f * gfs + cc[h]];
+        }
+        if (STAGE == 3) qu[h] = a.s.q[cc[h]];
+        if (STAGE == 4) {
+#pragma unroll
+          for (int f = 1; f <= 4; ++f) Qv[h][f] = a.s.q[f * gfs + cc[h]];
+          qu[h] = a.s.q[cc[h]];
+          yu[h] = a.s.y[cc[h]];
+        }
+      }
+    }
+    mbar_wait(zfull + (t + 2 * W) % Cf::RZ, ((t + 2 * W) / Cf::RZ) & 1);
+    mbar_wait(pfull + t % Cf::RP, (t / Cf::RP) & 1);
+    const double* zr[2 * W + 1];
+    const double* zv[2 * W + 1];
+#pragma unroll
+    for (int q = 0; q <= 2 * W; ++q) {
+      const unsigned char* sl = zbase + ((t + q) % Cf::RZ) * Cf::ZSLOT;
+      zr[q] = reinterpret_cast<const double*>(sl);
+      zv[q] = reinterpret_cast<const double*>(sl + Cf::ZRHO_B);
+    }
+    const unsigned char* ps = pbase + (t % Cf::RP) * Cf::PSLOT;
+    const double* sv1 = reinterpret_cast<const double*>(ps);
+    const double* sv2 = reinterpret_cast<const double*>(ps + Cf::PV1_B);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ty = warp + 8 * h;
+      const int cr = (ty + W) * Cf::RX + (lane + W);  // rho box index
+      const int cv = ty * Cf::TX + lane;              // centre box index
+      double S[5], kk[5];
+      S[GRHO] = zr[W][cr];
+      S[GV1] = sv1[ty * Cf::RX + lane + W];
+      S[GV2] = sv2[(ty + W) * Cf::TX + lane];
+      S[GV3] = zv[W][cv];
+      double dzr = 0.0, dv3 = 0.0;
+#pragma unroll
+      for (int q = W; q >= 1; --q) {
+        dzr = fma(D1W<W>::c(q), zr[W + q][cr] - zr[W - q][cr], dzr);
+        dv3 = fma(D1W<W>::c(q), zv[W + q][cv] - zv[W - q][cv], dv3);
+      }
+      const double dxr = d1s<W>(zr[W], cr, 1) * K.ih[0];
+      const double dyr = d1s<W>(zr[W], cr, Cf::RX) * K.ih[1];
+      dzr = dzr * K.ih[2];
+      const double dv1 = d1s<W>(sv1, ty * Cf::RX + lane + W, 1) * K.ih[0];
+      const double dv2 = d1s<W>(sv2, (ty + W) * Cf::TX + lane, Cf::TX) * K.ih[1];
+      dv3 = dv3 * K.ih[2];
+      kk[GRHO] = dv1 + dv2 + dv3;
+      kk[GV1] = dxr;
+      kk[GV2] = dyr;
+      kk[GV3] = dzr;
+      if (STAGE == 1) {
+#pragma unroll
+        for (int f = 1; f <= 4; ++f) Y[h][f] = S[f];
+      }
+      if (live[h]) {
+        const int j = j0 + ty;
+        const int64_t c = cc[h];
+        const bool nf = near_face(L, i, j, k);
+        auto put = [&](int f, double v) {
+          out[f * gfs + c] = v;
+          if (nf) store_images(out + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+          if (STAGE == 4) check_finite(a.nan_flag, code0 + f, v);
+        };
+        auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
+        wave_update<STAGE>(K, S, kk, Y[h], Qv[h], yu[h], qu[h], put, putq);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(pempty + t % Cf::RP);
+      mbar_arrive(zempty + t % Cf::RZ);  // plane k - W is no longer needed
+    }
+  }
+}
+
+template <int STAGE, int W>
+cudaError_t launch_tma(const StageLaunch& a, const WaveK& K, cudaStream_t st) {
+  using Cf = TmaCfg<W>;
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  const Layout& L = a.L;
+  const double* in = STAGE == 1 ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b));
+  const double* base = in - L.c0;
+  CUtensorMap mR, mV1, mV2, mC;
+  if (!encode_set_map(&mR, base, L.px, L.py, L.pz, L.n_gf, L.gfs, Cf::RX, Cf::RY) ||
+      !encode_set_map(&mV1, base, L.px, L.py, L.pz, L.n_gf, L.gfs, Cf::RX, Cf::TY) ||
+      !encode_set_map(&mV2, base, L.px, L.py, L.pz, L.n_gf, L.gfs, Cf::TX, Cf::RY) ||
+      !encode_set_map(&mC, base, L.px, L.py, L.pz, L.n_gf, L.gfs, Cf::TX, Cf::TY))
+    return cudaErrorInvalidValue;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(wave_tma<STAGE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const int tiles = (int)(((L.nx + Cf::TX - 1) / Cf::TX) * ((L.ny + Cf::TY - 1) / Cf::TY));
+  // ~64-plane chunks, but at least ~8 waves of 2 CTAs x 148 SMs when the tile count is small
+  int nchunks = (nk + 63) / 64;
+  const int want = (8 * 2 * 148 + tiles - 1) / tiles;
+  if (nchunks < want) nchunks = want;
+  int chunk = (nk + nchunks - 1) / nchunks;
+  if (chunk < 4) chunk = 4;
+  if (chunk > nk) chunk = nk;
+  nchunks = (nk + chunk - 1) / chunk;
+  dim3 grid((unsigned)((L.nx + Cf::TX - 1) / Cf::TX), (unsigned)((L.ny + Cf::TY - 1) / Cf::TY), (unsigned)nchunks);
+  wave_tma<STAGE, W><<<grid, 32 * (Cf::NCW + 1), Cf::SMEM, st>>>(mR, mV1, mV2, mC, a, K, chunk);
+  return cudaGetLastError();
+}
+
 WaveK make_k(const StageLaunch& a) {
   WaveK K;
   for (int d = 0; d < 3; ++d) K.ih[d] = 1.0 / a.h[d];
@@ -264,7 +492,16 @@ WaveK make_k(const StageLaunch& a) {
 template <int W>
 cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
   const WaveK K = make_k(a);
-  // variant 0 (default) and 1: one thread per point; 2: register-queue z-march
+  // variant 0 (default): TMA z-march (W <= 2); 1: one thread per point; 2: register-queue
+  // z-march.  Wider stencils and the RHS-only call use the one-thread-per-point kernel.
+  if (a.variant == 0 && W <= 2) {
+    switch (stage) {
+      case 1: return launch_tma<1, W>(a, K, st);
+      case 2: return launch_tma<2, W>(a, K, st);
+      case 3: return launch_tma<3, W>(a, K, st);
+      case 4: return launch_tma<4, W>(a, K, st);
+    }
+  }
   if (a.variant == 2) {
     switch (stage) {
       case 1: return launch_zmarch<1, W>(a, K, st);
@@ -294,6 +531,28 @@ cudaError_t dispatch(const StageLaunch& a, int stage, double* dst, cudaStream_t 
 }
 
 }  // namespace
+
+bool encode_set_map(CUtensorMap* out, const double* set_base, int64_t px, int64_t py, int64_t pz,
+                    int64_t n_gf, int64_t gfs, unsigned bx, unsigned by) {
+  typedef CUresult (*PFN_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static PFN_encode fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+      return false;
+    fn = reinterpret_cast<PFN_encode>(f);
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)px, (cuuint64_t)py, (cuuint64_t)pz, (cuuint64_t)n_gf};
+  const cuuint64_t strides[3] = {(cuuint64_t)(px * 8), (cuuint64_t)(px * py * 8), (cuuint64_t)(gfs * 8)};
+  const cuuint32_t box[4] = {bx, by, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(set_base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 cudaError_t wave_stage(const StageLaunch& a, int stage, cudaStream_t st) {
   return dispatch(a, stage, nullptr, st);
