@@ -68,6 +68,7 @@ struct chemora_grid_s {
   bool ipc;                     // neighbours are other processes (signal through flags)
   std::vector<void*> opened;    // IPC mappings to close
   int variant;
+  int band;                     // wave CTA band order (-1 auto; CHEMORA_WAVE_BAND)
 };
 
 namespace {
@@ -236,6 +237,7 @@ StageLaunch stage_args(chemora_grid_t g, double dt) {
   a.k_begin = 0;
   a.k_end = (int)g->L.nz;
   a.variant = g->variant;
+  a.band = g->band;
   return a;
 }
 
@@ -344,6 +346,9 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->variant = 0;
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
+  g->band = -1;
+  const char* bnd = getenv("CHEMORA_WAVE_BAND");
+  if (bnd) g->band = atoi(bnd);
   unsigned long long init[3] = {~0ull, 0ull, 0ull};
   cudaError_t e = cudaMemcpy(g->dparams, g->params, sizeof(g->params), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(fl, init, sizeof(init), cudaMemcpyHostToDevice);

@@ -36,6 +36,7 @@ struct StageLaunch {
   uint64_t step;         // global step index (for the non-finite report)
   int k_begin, k_end;    // local z-plane range [k_begin, k_end)
   int variant;           // kernel variant (0 = default fast, 1 = simple reference kernel)
+  int band;              // wave simple-kernel CTA band order (-1 auto, 0 plain 3-D order)
 };
 
 // Wave (Eq. 1) -------------------------------------------------------------------------

@@ -79,12 +79,31 @@ __device__ __forceinline__ void wave_update(const WaveK& K, const double* S, con
 // One thread per interior point, every stencil operand loaded through the read-only
 // path.  Used for RHS-only evaluation, as the variant-1 reference for tile-independence
 // tests, and as the fallback for shapes the tiled kernel does not take.
+//
+// CTA order (`band` > 0): a 1-D grid walked as (x-tile fastest, then `band` y-tiles, then z,
+// then the next group of y-tiles).  The CTAs resident at any moment then cover a band of
+// band*8 rows over a few consecutive planes, so the z-stencil planes (k +- 1, 2) and the
+// y-halo rows are re-read from L2 (a few MB of working set) instead of HBM.  With band = 0
+// the grid is the plain 3-D (x-tile, y-tile, z) launch.
 template <int STAGE, int W>
-__global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, double* rhs_dst) {
+__global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, double* rhs_dst, int band) {
   const Layout& L = a.L;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const int k = a.k_begin + blockIdx.z;
+  int bx, by, bz;
+  if (band > 0) {
+    const int ntx = (int)((L.nx + 31) >> 5), nty = (int)((L.ny + 7) >> 3);
+    const int nk = a.k_end - a.k_begin;
+    int lin = blockIdx.x;
+    bx = lin % ntx; lin /= ntx;
+    const int byl = lin % band; lin /= band;
+    bz = lin % nk;
+    by = (lin / nk) * band + byl;
+    if (by >= nty) return;
+  } else {
+    bx = blockIdx.x; by = blockIdx.y; bz = blockIdx.z;
+  }
+  const int i = bx * blockDim.x + threadIdx.x;
+  const int j = by * blockDim.y + threadIdx.y;
+  const int k = a.k_begin + bz;
   if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
   const int64_t c = L.idx(i, j, k);
   const int64_t gfs = L.gfs;
@@ -249,8 +268,23 @@ cudaError_t launch_simple(const StageLaunch& a, const WaveK& K, double* dst, cud
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
   dim3 block(32, 8, 1);
-  dim3 grid((unsigned)((a.L.nx + 31) / 32), (unsigned)((a.L.ny + 7) / 8), (unsigned)nk);
-  wave_simple<STAGE, W><<<grid, block, 0, st>>>(a, K, dst);
+  const int ntx = (int)((a.L.nx + 31) / 32), nty = (int)((a.L.ny + 7) / 8);
+  int band = a.band;
+  if (band < 0) {
+    // auto: keep ~5 planes x 17 streams of the band under ~40 MB of L2
+    const double rows = 40e6 / (5.0 * 17.0 * 8.0 * (double)a.L.nx);
+    band = 1;
+    while (band * 2 * 8 <= rows && band * 2 <= nty) band *= 2;
+  }
+  if (STAGE == 0 || a.variant == 1) band = 0;
+  if (band > 0) {
+    const int groups = (nty + band - 1) / band;
+    const long long n = (long long)ntx * band * nk * groups;
+    wave_simple<STAGE, W><<<dim3((unsigned)n), block, 0, st>>>(a, K, dst, band);
+  } else {
+    dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nk);
+    wave_simple<STAGE, W><<<grid, block, 0, st>>>(a, K, dst, 0);
+  }
   return cudaGetLastError();
 }
 
@@ -492,9 +526,11 @@ WaveK make_k(const StageLaunch& a) {
 template <int W>
 cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
   const WaveK K = make_k(a);
-  // variant 0 (default): TMA z-march (W <= 2); 1: one thread per point; 2: register-queue
-  // z-march.  Wider stencils and the RHS-only call use the one-thread-per-point kernel.
-  if (a.variant == 0 && W <= 2) {
+  // variant 0 (default) and 1: one thread per point (0: banded CTA order, 1: plain order);
+  // 2: register-queue z-march; 3: TMA z-march (W <= 2).  RHS-only uses the simple kernel.
+  if (a.variant == 3 && W <= 2) {
+
+
     switch (stage) {
       case 1: return launch_tma<1, W>(a, K, st);
       case 2: return launch_tma<2, W>(a, K, st);
