@@ -42,6 +42,8 @@ struct StageLaunch {
 // Wave (Eq. 1) -------------------------------------------------------------------------
 cudaError_t wave_stage(const StageLaunch& a, int stage, cudaStream_t st);
 cudaError_t wave_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
+// persistent TMA z-march (wave_tma.cu), fd_order 2 or 4, stages 1..4
+cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st);
 
 // BSSN (App. A) ------------------------------------------------------------------------
 cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st);

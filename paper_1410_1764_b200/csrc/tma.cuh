@@ -56,8 +56,9 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 }
 
 // Host: encode a 4-D fp64 tensor map over a state set [n_gf][pz][py][px] (x fastest) with a
-// (bx, by, 1, 1) box.  Returns false if the driver entry point or the encode fails.
+// (bx, by, 1, bg) box (bg consecutive GFs per load).  Returns false if the driver entry
+// point or the encode fails.
 bool encode_set_map(CUtensorMap* out, const double* set_base, int64_t px, int64_t py, int64_t pz,
-                    int64_t n_gf, int64_t gfs, unsigned bx, unsigned by);
+                    int64_t n_gf, int64_t gfs, unsigned bx, unsigned by, unsigned bg = 1);
 
 }  // namespace chemora

@@ -170,7 +170,7 @@ def test_kernel_variants_bitwise_identical():
     P, C = _mods()
     n = (70, 45, 33)
     out = []
-    for v in (0, 1, 2, 3):
+    for v in (0, 1, 2, 3, 4):
         g, h = grid(n)
         g.set_kernel_variant(v)
         g.set_initial(C.INIT_NOISE, seed=2)
@@ -179,6 +179,7 @@ def test_kernel_variants_bitwise_identical():
     assert np.array_equal(out[0], out[1])
     assert np.array_equal(out[0], out[2])
     assert np.array_equal(out[0], out[3])
+    assert np.array_equal(out[0], out[4])
 
 
 def _box_oracle_one_step(gext, h, dt, seed, center, R=10):
