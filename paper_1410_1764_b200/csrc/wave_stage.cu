@@ -13,6 +13,7 @@
 // for a z-slab, stores its boundary planes into the neighbour's ghost planes.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "grid.hpp"
 #include "kernels.hpp"
 #include "device_common.cuh"
@@ -534,9 +535,18 @@ bool encode_set_map(CUtensorMap* out, const double* set_base, int64_t px, int64_
   const cuuint64_t dims[4] = {(cuuint64_t)px, (cuuint64_t)py, (cuuint64_t)pz, (cuuint64_t)n_gf};
   const cuuint64_t strides[3] = {(cuuint64_t)(px * 8), (cuuint64_t)(px * py * 8), (cuuint64_t)(gfs * 8)};
   const cuuint32_t box[4] = {bx, by, 1, bg};
+  // L2 promotion: interior rows start on 128-byte (not 256-byte) boundaries, so 256-byte
+  // promotion would fetch a neighbour tile's half line with every row (measured: up to 2x
+  // DRAM reads).  Default: no promotion; CHEMORA_TMA_PROMO=0..3 selects NONE/64/128/256 B.
+  static int promo_sel = -1;
+  if (promo_sel < 0) {
+    const char* e = getenv("CHEMORA_TMA_PROMO");
+    promo_sel = e ? atoi(e) : 0;
+  }
+  const CUtensorMapL2promotion promo = (CUtensorMapL2promotion)promo_sel;
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(set_base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
