@@ -7,6 +7,7 @@ import numpy as np
 import torch
 
 from . import capi as C
+from . import dist as D
 
 
 def _stream_ptr(device) -> int:
@@ -71,20 +72,14 @@ class Grid:
     def norms(self, group=None):
         if self.nranks == 1:
             return C.chemora_norms(self.handle, self.system, self.stream)
-        import torch.distributed as dist
         part = C.chemora_norms_partial(self.handle, self.system, self.stream)
-        gathered = [None] * self.nranks
-        dist.all_gather_object(gathered, part.tolist(), group=group)
-        return C.chemora_norms_combine(self.desc, np.array(gathered), self.nranks)
+        gathered = D.gather_partials(part, self.nranks, group)
+        return C.chemora_norms_combine(self.desc, gathered, self.nranks)
 
     def connect_ipc(self, group=None):
         """Exchange peer records over torch.distributed and open the ring neighbours."""
-        import torch.distributed as dist
         rec = C.chemora_grid_export_peer(self.handle)
-        allrec = [None] * self.nranks
-        dist.all_gather_object(allrec, rec, group=group)
-        lo = allrec[(self.rank - 1) % self.nranks]
-        hi = allrec[(self.rank + 1) % self.nranks]
+        lo, hi = D.exchange_records(rec, self.rank, self.nranks, group)
         C.chemora_grid_connect_ipc(self.handle, lo, hi)
 
     def set_kernel_variant(self, v):
