@@ -44,9 +44,10 @@ def lib():
         dp = ctypes.POINTER(ctypes.c_double)
         i64p = ctypes.POINTER(ctypes.c_int64)
         L.chemora_oracle_fill_ghosts.argtypes = [dp, ctypes.c_int, i64p, ctypes.c_int]
-        L.chemora_oracle_rhs.argtypes = [ctypes.c_int, dp, dp, i64p, ctypes.c_int, dp, dp]
-        L.chemora_oracle_rk4.argtypes = [ctypes.c_int, dp, i64p, ctypes.c_int, dp,
-                                         ctypes.c_double, ctypes.c_int, dp]
+        L.chemora_oracle_rhs_order.argtypes = [ctypes.c_int, dp, dp, i64p, ctypes.c_int, dp, dp,
+                                               ctypes.c_int]
+        L.chemora_oracle_rk4_order.argtypes = [ctypes.c_int, dp, i64p, ctypes.c_int, dp,
+                                               ctypes.c_double, ctypes.c_int, dp, ctypes.c_int]
         L.chemora_oracle_norms.argtypes = [ctypes.c_int, dp, i64p, ctypes.c_int, dp, dp]
         L.chemora_oracle_default_bssn_params.argtypes = [dp]
         _lib = L
@@ -105,33 +106,34 @@ def fill_ghosts(padded: np.ndarray, g: int = DEFAULT_GHOST) -> np.ndarray:
 
 
 def rhs_padded(system: int, padded: np.ndarray, spacing, params=None,
-               g: int = DEFAULT_GHOST) -> np.ndarray:
+               g: int = DEFAULT_GHOST, order: int = 4) -> np.ndarray:
     """k = F(y) on the interior, ghosts of ``padded`` used as they are."""
     padded = np.ascontiguousarray(padded, dtype=np.float64)
     n = (padded.shape[3] - 2 * g, padded.shape[2] - 2 * g, padded.shape[1] - 2 * g)
     k = np.zeros((padded.shape[0], n[2], n[1], n[0]))
     p = _params(params)
-    rc = lib().chemora_oracle_rhs(system, _dp(padded), _dp(k), _ext(n), g, _sp(spacing),
-                                  _dp(p) if p is not None else None)
+    rc = lib().chemora_oracle_rhs_order(system, _dp(padded), _dp(k), _ext(n), g, _sp(spacing),
+                                        _dp(p) if p is not None else None, order)
     if rc:
         raise ValueError(f"oracle rhs rc={rc}")
     return k
 
 
-def rhs(system: int, interior: np.ndarray, spacing, params=None, g: int = DEFAULT_GHOST):
-    """k = F(y) on a periodic grid (ghosts filled first)."""
+def rhs(system: int, interior: np.ndarray, spacing, params=None, g: int = DEFAULT_GHOST,
+        order: int = 4):
+    """k = F(y) on a periodic grid (ghosts filled first).  ``order``: wave D1 accuracy."""
     p = fill_ghosts(pad(interior, g), g)
-    return rhs_padded(system, p, spacing, params, g)
+    return rhs_padded(system, p, spacing, params, g, order)
 
 
 def rk4(system: int, interior: np.ndarray, spacing, dt: float, nsteps: int, params=None,
-        g: int = DEFAULT_GHOST) -> np.ndarray:
+        g: int = DEFAULT_GHOST, order: int = 4) -> np.ndarray:
     """``nsteps`` textbook RK4 steps on a periodic grid; returns the new interior."""
     y = pad(np.ascontiguousarray(interior, dtype=np.float64), g)
     n = extent_of(interior)
     p = _params(params)
-    rc = lib().chemora_oracle_rk4(system, _dp(y), _ext(n), g, _sp(spacing), float(dt),
-                                  int(nsteps), _dp(p) if p is not None else None)
+    rc = lib().chemora_oracle_rk4_order(system, _dp(y), _ext(n), g, _sp(spacing), float(dt),
+                                        int(nsteps), _dp(p) if p is not None else None, order)
     if rc:
         raise ValueError(f"oracle rk4 rc={rc}")
     return unpad(y, g)

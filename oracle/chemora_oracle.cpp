@@ -40,6 +40,7 @@ struct Grid {
   int g;          // ghost width
   int64_t p[3];   // padded extents
   double h[3];
+  int order = 4;  // accuracy order of the wave system's centered D1 (2, 4, 6, 8)
   Grid(const int64_t* ext, int ghost, const double* sp) {
     for (int a = 0; a < 3; ++a) { n[a] = ext[a]; p[a] = ext[a] + 2 * ghost; h[a] = sp[a]; }
     g = ghost;
@@ -88,6 +89,24 @@ void fill_ghosts_one(double* f, const Grid& G) {
 //   D1 f = (f[-2] - 8 f[-1] + 8 f[+1] - f[+2]) / (12 h)        (SPEC.md:218 (d=1,w=2))
 inline double d1(const double* f, int64_t c, int64_t s, double h) {
   return (f[c - 2 * s] - 8.0 * f[c - s] + 8.0 * f[c + s] - f[c + 2 * s]) / (12.0 * h);
+}
+// Centered first derivatives of order 2, 6 and 8 (the standard operators of PAPER.md:
+// 509-514, "Finite Differencing with arbitrary order of accuracy ... run-time option";
+// SURVEY.md §8(f) NEXT-1), written out literally:
+//   order 2: (f[+1] - f[-1]) / (2h)
+//   order 6: (-f[-3] + 9f[-2] - 45f[-1] + 45f[+1] - 9f[+2] + f[+3]) / (60h)
+//   order 8: (3f[-4] - 32f[-3] + 168f[-2] - 672f[-1] + 672f[+1] - 168f[+2] + 32f[+3] - 3f[+4]) / (840h)
+inline double d1n(const double* f, int64_t c, int64_t s, double h, int order) {
+  switch (order) {
+    case 2: return (f[c + s] - f[c - s]) / (2.0 * h);
+    case 6:
+      return (-f[c - 3 * s] + 9.0 * f[c - 2 * s] - 45.0 * f[c - s] + 45.0 * f[c + s] - 9.0 * f[c + 2 * s] +
+              f[c + 3 * s]) / (60.0 * h);
+    case 8:
+      return (3.0 * f[c - 4 * s] - 32.0 * f[c - 3 * s] + 168.0 * f[c - 2 * s] - 672.0 * f[c - s] +
+              672.0 * f[c + s] - 168.0 * f[c + 2 * s] + 32.0 * f[c + 3 * s] - 3.0 * f[c + 4 * s]) / (840.0 * h);
+    default: return d1(f, c, s, h);
+  }
 }
 // Centered 4th-order second derivative:
 //   D2 f = (-f[-2] + 16 f[-1] - 30 f[0] + 16 f[+1] - f[+2]) / (12 h^2)
@@ -140,10 +159,11 @@ void wave_rhs(const double* y, double* k, const Grid& G) {
       for (int64_t i = 0; i < G.n[0]; ++i) {
         const int64_t c = G.at(i, j, kk), o = G.at_int(i, j, kk);
         k[0 * ni + o] = rho[c];
-        k[1 * ni + o] = d1(v1, c, sx, G.h[0]) + d1(v2, c, sy, G.h[1]) + d1(v3, c, sz, G.h[2]);
-        k[2 * ni + o] = d1(rho, c, sx, G.h[0]);
-        k[3 * ni + o] = d1(rho, c, sy, G.h[1]);
-        k[4 * ni + o] = d1(rho, c, sz, G.h[2]);
+        const int q = G.order;
+        k[1 * ni + o] = d1n(v1, c, sx, G.h[0], q) + d1n(v2, c, sy, G.h[1], q) + d1n(v3, c, sz, G.h[2], q);
+        k[2 * ni + o] = d1n(rho, c, sx, G.h[0], q);
+        k[3 * ni + o] = d1n(rho, c, sy, G.h[1], q);
+        k[4 * ni + o] = d1n(rho, c, sz, G.h[2], q);
       }
 }
 
@@ -438,23 +458,35 @@ int chemora_oracle_fill_ghosts(double* f, int n_gf, const int64_t* ext, int g) {
 }
 
 // k = F(y) at interior points, ghosts of y used as they are.  y: padded, k: interior.
-int chemora_oracle_rhs(int system, const double* y, double* k, const int64_t* ext, int g,
-                       const double* spacing, const double* params) {
+// fd_order: accuracy order of the wave system's centered D1 (2, 4, 6, 8); BSSN: 4 only.
+int chemora_oracle_rhs_order(int system, const double* y, double* k, const int64_t* ext, int g,
+                             const double* spacing, const double* params, int fd_order) {
   if (n_gf_of(system) < 0) return 1;
-  if (g < (system == 1 ? 2 : 3)) return 2;
+  if (fd_order != 2 && fd_order != 4 && fd_order != 6 && fd_order != 8) return 3;
+  if (system == 2 && fd_order != 4) return 3;
+  if (g < (system == 1 ? fd_order / 2 : 3)) return 2;
   Grid G(ext, g, spacing);
+  G.order = fd_order;
   rhs_any(system, y, k, G, params);
   return 0;
 }
 
+int chemora_oracle_rhs(int system, const double* y, double* k, const int64_t* ext, int g,
+                       const double* spacing, const double* params) {
+  return chemora_oracle_rhs_order(system, y, k, ext, g, spacing, params, 4);
+}
+
 // nsteps classical RK4 steps in place on the padded state y (textbook k1..k4 form).
 // On return the ghosts of y are filled.
-int chemora_oracle_rk4(int system, double* y, const int64_t* ext, int g, const double* spacing,
-                       double dt, int nsteps, const double* params) {
+int chemora_oracle_rk4_order(int system, double* y, const int64_t* ext, int g, const double* spacing,
+                             double dt, int nsteps, const double* params, int fd_order) {
   const int nf = n_gf_of(system);
   if (nf < 0) return 1;
-  if (g < (system == 1 ? 2 : 3)) return 2;
+  if (fd_order != 2 && fd_order != 4 && fd_order != 6 && fd_order != 8) return 3;
+  if (system == 2 && fd_order != 4) return 3;
+  if (g < (system == 1 ? fd_order / 2 : 3)) return 2;
   Grid G(ext, g, spacing);
+  G.order = fd_order;
   const int64_t np = G.npad(), ni = G.nint();
   std::vector<double> Y(static_cast<size_t>(nf * np));
   std::vector<double> k1(nf * ni), k2(nf * ni), k3(nf * ni), k4(nf * ni);
@@ -491,6 +523,11 @@ int chemora_oracle_rk4(int system, double* y, const int64_t* ext, int g, const d
   }
   fill(y);
   return 0;
+}
+
+int chemora_oracle_rk4(int system, double* y, const int64_t* ext, int g, const double* spacing,
+                       double dt, int nsteps, const double* params) {
+  return chemora_oracle_rk4_order(system, y, ext, g, spacing, dt, nsteps, params, 4);
 }
 
 // Norms over the interior: out[3*v+0] = L2 = sqrt(h^3 sum f^2),

@@ -92,3 +92,32 @@ def discrete_plane_wave(n, h, dt, nsteps, modes):
         for f in range(5):
             out[f] += (cn[f] * e).real
     return out
+
+
+def ktilde(k: float, h: float, order: int) -> float:
+    """Fourier symbol of the centered D1 of accuracy ``order``: D1 e^{ikx} = i ktilde e^{ikx},
+    ktilde = sum_{s>0} 2 c_s sin(s k h) / h with c_s from the exact moment solve."""
+    w = order // 2
+    c = moment_solve(1, range(-w, w + 1))
+    return sum(2.0 * float(c[w + s]) * math.sin(s * k * h) for s in range(1, w + 1)) / h
+
+
+def discrete_plane_wave_order(n, h, dt, nsteps, modes, order):
+    """discrete_plane_wave for a centered D1 of any even accuracy order."""
+    nx, ny, nz = n
+    x = np.arange(nx)[None, None, :] * h[0]
+    y = np.arange(ny)[None, :, None] * h[1]
+    z = np.arange(nz)[:, None, None] * h[2]
+    out = np.zeros((5, nz, ny, nx))
+    for (kx, ky, kz), a, ph in modes:
+        w = math.sqrt(kx * kx + ky * ky + kz * kz)
+        c = np.exp(1j * ph) * np.array([-1j * a, -a * w, a * kx, a * ky, a * kz], dtype=complex)
+        M = np.zeros((5, 5), dtype=complex)
+        M[0, 1] = 1.0
+        for j, (kk, hh) in enumerate(zip((kx, ky, kz), h)):
+            M[1, 2 + j] = M[2 + j, 1] = 1j * ktilde(kk, hh, order)
+        cn = np.linalg.matrix_power(rk4_poly(dt * M), nsteps) @ c
+        e = np.exp(1j * (kx * x + ky * y + kz * z))
+        for f in range(5):
+            out[f] += (cn[f] * e).real
+    return out

@@ -225,3 +225,22 @@ def test_full_size_512_sampled_parity():
     for f in (1, 2, 3, 4):
         assert abs(n1[3 * f + 2] - n0[3 * f + 2]) <= 1e-6 * vol
     assert n1[-1] <= n0[-1]  # energy non-increasing
+
+
+@pytest.mark.parametrize("order", [2, 4, 6, 8])
+def test_fd_order_parity(order):
+    """NEXT-1: run-time selectable accuracy order, every tiling."""
+    P, C = _mods()
+    n = (40, 36, 44)
+    h = tuple(2 * math.pi / v for v in n)
+    dt = 0.2 * min(h)
+    y0 = ci.noise(n, 5, seed=order)
+    ref = oracle.rk4(W, y0, h, dt, 10, g=4, order=order)
+    for v in (0, 4):
+        g = P.Grid(C.SYS_WAVE, n, h, ghost=4, fd_order=order)
+        g.set_kernel_variant(v)
+        g.set_initial(C.INIT_HOST, y0)
+        g.rk4_step(dt, 10)
+        assert relerr(g.get_state(), ref) <= 1e-12
+        k = g.rhs().cpu().numpy()
+        assert relerr(k, oracle.rhs(W, y0, h, g=4, order=order)) <= 1e-13
