@@ -479,7 +479,7 @@ cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStr
   // variant 0 (default) and 1: one thread per point (0: banded CTA order, 1: plain order);
   // 2: register-queue z-march; 3: TMA z-march (W <= 2).  RHS-only uses the simple kernel.
   if (a.variant == 4 && W <= 2 && stage >= 1) return wave_tma_stage(a, stage, st);
-  if (a.variant == 3 && W <= 2) {
+  if (a.variant == 3 && W == 2) {
 
 
     switch (stage) {

@@ -18,6 +18,7 @@
 // (bit-identical results; compiled without FMA contraction).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "grid.hpp"
 #include "kernels.hpp"
 #include "device_common.cuh"
@@ -40,7 +41,10 @@ template <int STAGE> struct PW {
 template <int STAGE, int W>
 struct Cfg {
   static constexpr int TX = 32, TY = 16, NCW = 16;
-  static constexpr int RX = TX + 2 * W, RY = TY + 2 * W;
+  // box halo: the stencil radius rounded up to even, because a TMA box must start on a
+  // 16-byte boundary in x (an odd fp64 offset raises an illegal-instruction fault)
+  static constexpr int H = (W + 1) / 2 * 2;
+  static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
   static constexpr int RZ = 2 * W + 3, RP = 3;
   static constexpr int C = TX * TY;  // points per tile plane
   static constexpr int ZRHO_B = r128(RX * RY * 8), ZV3_B = r128(C * 8), ZSLOT = ZRHO_B + ZV3_B;
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
         unsigned char* dst = zbase + s * Cf::ZSLOT;
         const int zc = g + plane;
         mbar_arrive_expect_tx(zfull + s, Cf::ZBYTES);
-        tma_load_4d(dst, &M.rho, zfull + s, kXOff + i0 - W, g + j0 - W, zc, GRHO);
+        tma_load_4d(dst, &M.rho, zfull + s, kXOff + i0 - Cf::H, g + j0 - Cf::H, zc, GRHO);
         tma_load_4d(dst + Cf::ZRHO_B, &M.c1, zfull + s, kXOff + i0, g + j0, zc, GV3);
         ++nz;
       };
@@ -125,8 +129,8 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
         const int zc = g + plane;
         uint64_t* bar = pfull + s;
         mbar_arrive_expect_tx(bar, Cf::PBYTES);
-        tma_load_4d(dst, &M.v1, bar, kXOff + i0 - W, g + j0, zc, GV1);
-        tma_load_4d(dst + Cf::PV1_B, &M.v2, bar, kXOff + i0, g + j0 - W, zc, GV2);
+        tma_load_4d(dst, &M.v1, bar, kXOff + i0 - Cf::H, g + j0, zc, GV1);
+        tma_load_4d(dst + Cf::PV1_B, &M.v2, bar, kXOff + i0, g + j0 - Cf::H, zc, GV2);
         unsigned char* d2 = dst + Cf::PV1_B + Cf::PV2_B;
         if (P::NY) tma_load_4d(d2, &M.y4, bar, kXOff + i0, g + j0, zc, GRHO);
         if (P::NQ) tma_load_4d(d2 + Cf::PY_B, &M.q, bar, kXOff + i0, g + j0, zc, GU);
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
   const FaceDst fd = a.img[STAGE - 1];
   const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
   const int ty = warp, tx = lane;
-  const int cr = (ty + W) * Cf::RX + (tx + W);  // rho box index
+  const int cr = (ty + Cf::H) * Cf::RX + (tx + Cf::H);  // rho box index
   const int cv = ty * Cf::TX + tx;              // centre box index
   uint32_t nz = 0, np = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -181,8 +185,8 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
       const double* su = reinterpret_cast<const double*>(ps + Cf::PV1_B + Cf::PV2_B + Cf::PY_B + Cf::PQ_B);
       double S[5], kk[5], Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
       S[GRHO] = zr[W][cr];
-      S[GV1] = sv1[ty * Cf::RX + tx + W];
-      S[GV2] = sv2[(ty + W) * Cf::TX + tx];
+      S[GV1] = sv1[ty * Cf::RX + tx + Cf::H];
+      S[GV2] = sv2[(ty + Cf::H) * Cf::TX + tx];
       S[GV3] = zv[W][cv];
       double dzr = 0.0, dv3 = 0.0;
 #pragma unroll
@@ -193,8 +197,8 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
       const double dxr = d1s<W>(zr[W], cr, 1) * K.ih[0];
       const double dyr = d1s<W>(zr[W], cr, Cf::RX) * K.ih[1];
       dzr = dzr * K.ih[2];
-      const double dv1 = d1s<W>(sv1, ty * Cf::RX + tx + W, 1) * K.ih[0];
-      const double dv2 = d1s<W>(sv2, (ty + W) * Cf::TX + tx, Cf::TX) * K.ih[1];
+      const double dv1 = d1s<W>(sv1, ty * Cf::RX + tx + Cf::H, 1) * K.ih[0];
+      const double dv2 = d1s<W>(sv2, (ty + Cf::H) * Cf::TX + tx, Cf::TX) * K.ih[1];
       dv3 = dv3 * K.ih[2];
       kk[GRHO] = dv1 + dv2 + dv3;
       kk[GV1] = dxr;
@@ -271,7 +275,13 @@ cudaError_t launch(const StageLaunch& a, const WaveK& K, cudaStream_t st) {
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntx = (int)((L.nx + Cf::TX - 1) / Cf::TX), nty = (int)((L.ny + Cf::TY - 1) / Cf::TY);
   // chunks of ~64 planes, but enough items for >= 8 per SM (load balance of the round robin)
-  int nchunks = (nk + 63) / 64;
+  static int chunk_env = -1;
+  if (chunk_env < 0) {
+    const char* e = getenv("CHEMORA_TMA_CHUNK");
+    chunk_env = e ? atoi(e) : 0;
+  }
+  const int target = chunk_env > 0 ? chunk_env : 64;
+  int nchunks = (nk + target - 1) / target;
   const int want = (8 * nsm + ntx * nty - 1) / (ntx * nty);
   if (nchunks < want) nchunks = want;
   int chunk = (nk + nchunks - 1) / nchunks;
