@@ -40,20 +40,20 @@ __global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, doubl
   const Layout& L = a.L;
   int bx, by, bz;
   if (band > 0) {
-    const int ntx = (int)((L.nx + 31) >> 5), nty = (int)((L.ny + 7) >> 3);
-    const int nk = a.k_end - a.k_begin;
+    const int ntx = (int)((L.nx + 31) >> 5), nty = (int)((L.ny + blockDim.y - 1) / blockDim.y);
+    const int ntz = (int)((a.k_end - a.k_begin + blockDim.z - 1) / blockDim.z);
     int lin = blockIdx.x;
     bx = lin % ntx; lin /= ntx;
     const int byl = lin % band; lin /= band;
-    bz = lin % nk;
-    by = (lin / nk) * band + byl;
+    bz = lin % ntz;
+    by = (lin / ntz) * band + byl;
     if (by >= nty) return;
   } else {
     bx = blockIdx.x; by = blockIdx.y; bz = blockIdx.z;
   }
   const int i = bx * blockDim.x + threadIdx.x;
   const int j = by * blockDim.y + threadIdx.y;
-  const int k = a.k_begin + bz;
+  const int k = a.k_begin + bz * blockDim.z + threadIdx.z;
   if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
   const int64_t c = L.idx(i, j, k);
   const int64_t gfs = L.gfs;
@@ -217,22 +217,32 @@ template <int STAGE, int W>
 cudaError_t launch_simple(const StageLaunch& a, const WaveK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
-  dim3 block(32, 8, 1);
-  const int ntx = (int)((a.L.nx + 31) / 32), nty = (int)((a.L.ny + 7) / 8);
+  // CTA shape 32 x BY x BZ (BY * BZ = 8): BZ > 1 keeps z-neighbour planes inside the CTA
+  // (L1 hits instead of L2 requests).  CHEMORA_WAVE_BZ selects BZ (1, 2, 4, 8).
+  static int bz_env = -1;
+  if (bz_env < 0) {
+    const char* e = getenv("CHEMORA_WAVE_BZ");
+    bz_env = e ? atoi(e) : 1;
+    if (bz_env != 1 && bz_env != 2 && bz_env != 4 && bz_env != 8) bz_env = 1;
+  }
+  const int BZ = (STAGE == 0 || a.variant == 1) ? 1 : bz_env, BY = 8 / BZ;
+  dim3 block(32, BY, BZ);
+  const int ntx = (int)((a.L.nx + 31) / 32), nty = (int)((a.L.ny + BY - 1) / BY);
+  const int ntz = (nk + BZ - 1) / BZ;
   int band = a.band;
   if (band < 0) {
     // auto: keep ~5 planes x 17 streams of the band under ~40 MB of L2
     const double rows = 40e6 / (5.0 * 17.0 * 8.0 * (double)a.L.nx);
     band = 1;
-    while (band * 2 * 8 <= rows && band * 2 <= nty) band *= 2;
+    while (band * 2 * BY <= rows && band * 2 <= nty) band *= 2;
   }
   if (STAGE == 0 || a.variant == 1) band = 0;
   if (band > 0) {
     const int groups = (nty + band - 1) / band;
-    const long long n = (long long)ntx * band * nk * groups;
+    const long long n = (long long)ntx * band * ntz * groups;
     wave_simple<STAGE, W><<<dim3((unsigned)n), block, 0, st>>>(a, K, dst, band);
   } else {
-    dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)nk);
+    dim3 grid((unsigned)ntx, (unsigned)nty, (unsigned)ntz);
     wave_simple<STAGE, W><<<grid, block, 0, st>>>(a, K, dst, 0);
   }
   return cudaGetLastError();
