@@ -14,6 +14,8 @@
 // S = (D+ + D-)/2 and A = (D+ - D-)/2 (identical to max(beta,0) D+ + min(beta,0) D-).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include "grid.hpp"
 #include "kernels.hpp"
 #include "device_common.cuh"
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, doubl
   const Layout& L = a.L;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const int k = a.k_begin + blockIdx.z;
+  const int k = a.k_begin + blockIdx.z * blockDim.z + threadIdx.z;
   if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
   const int64_t c = L.idx(i, j, k);
   const int64_t gfs = L.gfs;
@@ -460,8 +462,19 @@ template <int STAGE, int G>
 cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
-  dim3 block(32, 4, 1);
-  dim3 grid((unsigned)((a.L.nx + 31) / 32), (unsigned)((a.L.ny + 3) / 4), (unsigned)nk);
+  // CTA shape (128 threads): CHEMORA_BSSN_BLOCK = "BXxBYxBZ" (default 32x4x1).  A compact
+  // 3-D shape keeps more of each GF's stencil footprint inside the CTA (L1 hits).
+  static int bdim[3] = {0, 0, 0};
+  if (!bdim[0]) {
+    bdim[0] = 32; bdim[1] = 4; bdim[2] = 1;
+    if (const char* e = getenv("CHEMORA_BSSN_BLOCK")) {
+      int x, y, z;
+      if (sscanf(e, "%dx%dx%d", &x, &y, &z) == 3 && x * y * z == 128) { bdim[0] = x; bdim[1] = y; bdim[2] = z; }
+    }
+  }
+  dim3 block(bdim[0], bdim[1], bdim[2]);
+  dim3 grid((unsigned)((a.L.nx + bdim[0] - 1) / bdim[0]), (unsigned)((a.L.ny + bdim[1] - 1) / bdim[1]),
+            (unsigned)((nk + bdim[2] - 1) / bdim[2]));
   bssn_simple<STAGE, G><<<grid, block, 0, st>>>(a, K, dst);
   return cudaGetLastError();
 }
