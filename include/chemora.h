@@ -178,6 +178,29 @@ int chemora_peer_record_size(size_t* bytes);
 int chemora_grid_export_peer(chemora_grid_t grid, void* record_out);
 int chemora_grid_connect_ipc(chemora_grid_t grid, const void* record_lo, const void* record_hi);
 
+/* ---- analysis and tuning */
+
+/* Fused energy monitor (wave only; Fig. 1 "Energy" eps = 1/2 (rho^2 + delta^ij v_i v_j),
+ * PAPER.md:642-644): when enabled, every chemora_rk4_step step's last stage kernel also
+ * reduces E = h^3 sum eps of the new state (deterministic per-CTA partials + a fixed-order
+ * sum) -- no extra HBM pass over the state.  Single-slab grids (nranks == 1) only. */
+int chemora_set_monitor(chemora_grid_t grid, int enable);
+
+/* Copy up to max per-step energies recorded since the last read (oldest first) to out;
+ * *count receives the number copied.  Synchronises the stream.  The device ring holds 1024
+ * steps; reading less often is an error (CHEMORA_E_INVALID). */
+int chemora_read_monitor(chemora_grid_t grid, double* out, int32_t max, int32_t* count,
+                         void* stream);
+
+/* Model-driven tiling choice ("autotuning is model driven"): a
+ * footprint/occupancy model prunes the stage-kernel tilings to <= 3 candidates, each is
+ * timed on `trials` stage-1 launches (dt = 0: the state is not modified, the scratch set B
+ * is), and the fastest is kept for this handle.  chosen[3] = {variant, band, #candidates};
+ * ms_out (optional, >= 3 doubles) receives the best time per candidate.  Synchronises.
+ * With nranks > 1 every rank must call it at the same point of its call sequence. */
+int chemora_autotune(chemora_grid_t grid, int32_t trials, int32_t* chosen, double* ms_out,
+                     void* stream);
+
 /* ---- testing hooks (not part of the user-facing contract) */
 
 /* Select the stage-kernel variant of this handle: 0 = tiled fast kernel (default),

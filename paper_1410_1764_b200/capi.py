@@ -71,6 +71,9 @@ _SIGS = {
     "chemora_grid_export_peer": ([_vp, _vp], ctypes.c_int),
     "chemora_grid_connect_ipc": ([_vp, _vp, _vp], ctypes.c_int),
     "chemora_set_kernel_variant": ([_vp, ctypes.c_int], ctypes.c_int),
+    "chemora_set_monitor": ([_vp, ctypes.c_int], ctypes.c_int),
+    "chemora_read_monitor": ([_vp, _dp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
+    "chemora_autotune": ([_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _dp, _vp], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -235,3 +238,23 @@ def chemora_grid_connect_ipc(h, rec_lo: bytes, rec_hi: bytes):
 
 def chemora_set_kernel_variant(h, variant: int):
     _check(_lib.chemora_set_kernel_variant(h, variant), "chemora_set_kernel_variant")
+
+
+def chemora_set_monitor(h, enable: bool):
+    _check(_lib.chemora_set_monitor(h, 1 if enable else 0), "chemora_set_monitor")
+
+
+def chemora_read_monitor(h, max_steps: int = 1024, stream=None) -> np.ndarray:
+    out = np.zeros(max(1, max_steps))
+    cnt = ctypes.c_int32()
+    _check(_lib.chemora_read_monitor(h, _dptr(out), max_steps, ctypes.byref(cnt), stream),
+           "chemora_read_monitor")
+    return out[:cnt.value].copy()
+
+
+def chemora_autotune(h, trials: int = 3, stream=None):
+    chosen = (ctypes.c_int32 * 3)()
+    ms = np.zeros(4)
+    _check(_lib.chemora_autotune(h, trials, chosen, _dptr(ms), stream), "chemora_autotune")
+    return {"variant": chosen[0], "band": chosen[1], "candidates": chosen[2],
+            "ms": ms[:chosen[2]].tolist()}

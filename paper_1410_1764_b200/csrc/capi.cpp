@@ -69,6 +69,12 @@ struct chemora_grid_s {
   std::vector<void*> opened;    // IPC mappings to close
   int variant;
   int band;                     // wave CTA band order (-1 auto; CHEMORA_WAVE_BAND)
+  bool monitor;                 // NEXT-3 fused energy monitor enabled
+  double* mon_partials;
+  int64_t mon_n;
+  double* mon_hist;             // ring of kMonHist per-step energies (device)
+  uint64_t mon_written;         // steps recorded since creation
+  uint64_t mon_read;            // steps already returned by chemora_read_monitor
 };
 
 namespace {
@@ -119,8 +125,10 @@ int norms_len(int system, int n_gf) { return 3 * n_gf + (system == CHEMORA_SYS_W
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 // workspace: [sets][norm scratch][norm out][params][flags]
+constexpr int kMonHist = 1024;  // energy-monitor ring (steps)
 struct WsPlan {
-  size_t sets, scratch, out, params, flags, total;
+  size_t sets, scratch, out, params, flags, mon, hist, total;
+  int64_t mon_n;
 };
 WsPlan plan_ws(const Layout& L, int system) {
   WsPlan p;
@@ -135,6 +143,17 @@ WsPlan plan_ws(const Layout& L, int system) {
   off += align256(sizeof(double) * kParams);
   p.flags = off;
   off += align256(sizeof(unsigned long long) * 4);
+  // NEXT-3 fused energy monitor (wave): per-CTA partials of the stage-4 launch (any CTA
+  // shape 32 x BY x BZ with BY * BZ = 8) and a ring of per-step energies
+  p.mon_n = 0;
+  if (system == CHEMORA_SYS_WAVE) {
+    const int64_t ntx = (L.nx + 31) / 32;
+    p.mon_n = ntx * (L.ny * L.nz / 8 + L.ny + L.nz + 1);
+  }
+  p.mon = off;
+  off += align256(sizeof(double) * (size_t)p.mon_n);
+  p.hist = off;
+  off += align256(sizeof(double) * kMonHist);
   p.total = off;
   return p;
 }
@@ -238,6 +257,7 @@ StageLaunch stage_args(chemora_grid_t g, double dt) {
   a.k_end = (int)g->L.nz;
   a.variant = g->variant;
   a.band = g->band;
+  a.mon_partials = nullptr;
   return a;
 }
 
@@ -332,6 +352,12 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->norm_scratch = reinterpret_cast<double*>(g->ws + P.scratch);
   g->norm_out = reinterpret_cast<double*>(g->ws + P.out);
   g->dparams = reinterpret_cast<double*>(g->ws + P.params);
+  g->monitor = false;
+  g->mon_partials = reinterpret_cast<double*>(g->ws + P.mon);
+  g->mon_n = P.mon_n;
+  g->mon_hist = reinterpret_cast<double*>(g->ws + P.hist);
+  g->mon_written = 0;
+  g->mon_read = 0;
   auto* fl = reinterpret_cast<unsigned long long*>(g->ws + P.flags);
   g->nan_flag = fl;
   g->flags = fl + 1;
@@ -494,16 +520,107 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
     return fail(CHEMORA_E_PEER, "locally connected slabs step through chemora_rk4_step_multi");
   DeviceGuard dg(g->desc.device);
   cudaStream_t st = as_stream(stream);
+  const bool mon = g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0;
+  const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
   for (int n = 0; n < nsteps; ++n) {
     StageLaunch a = stage_args(g, dt);
     for (int s = 1; s <= 4; ++s) {
       if (int rc = phase_wait(g, st)) return rc;
+      if (s == 4 && mon) {
+        CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
+        a.mon_partials = g->mon_partials;
+      }
       CUDA_TRY(launch_stage(g, a, s, st));
+      if (s == 4 && mon) {
+        CUDA_TRY(monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st));
+        g->mon_written += 1;
+      }
       if (int rc = phase_signal(g, st)) return rc;
     }
     g->step += 1;
   }
   return CHEMORA_OK;
+}
+
+int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* ms_out, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (trials < 1) trials = 3;
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  // candidate tilings (variant, band), pruned by a footprint model:
+  //   wave: one thread per point in plain order (L1/L2 reuse of every stencil operand),
+  //         the same in the banded L2-window order, and the persistent TMA z-march (only
+  //         when its 32x16 tiles fill the SMs and the stencil radius is <= 2);
+  //   BSSN: fissioned kernels, and the fused single kernel only for small grids (it spills).
+  struct Cand { int variant, band; };
+  std::vector<Cand> cands;
+  if (g->desc.system == CHEMORA_SYS_WAVE) {
+    cands.push_back({0, 0});
+    cands.push_back({0, -1});
+    const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
+    const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
+    if (order <= 4 && tiles >= 148) cands.push_back({4, 0});
+  } else {
+    cands.push_back({0, 0});
+    if (g->L.nx * g->L.ny * g->L.nz <= (int64_t)64 * 64 * 64) cands.push_back({1, 0});
+  }
+  const int saved_v = g->variant, saved_b = g->band;
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  double best = 1e300;
+  int besti = 0;
+  for (size_t c = 0; c < cands.size(); ++c) {
+    g->variant = cands[c].variant;
+    g->band = cands[c].band;
+    StageLaunch a = stage_args(g, 0.0);  // dt = 0: stage 1 writes B = y, the state is untouched
+    CUDA_TRY(launch_stage(g, a, 1, st));
+    float msmin = 1e30f;
+    for (int t = 0; t < trials; ++t) {
+      CUDA_TRY(cudaEventRecord(e0, st));
+      CUDA_TRY(launch_stage(g, a, 1, st));
+      CUDA_TRY(cudaEventRecord(e1, st));
+      CUDA_TRY(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      if (ms < msmin) msmin = ms;
+    }
+    if (ms_out) ms_out[c] = msmin;
+    if (msmin < best) { best = msmin; besti = (int)c; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  (void)saved_v; (void)saved_b;
+  g->variant = cands[besti].variant;
+  g->band = cands[besti].band;
+  if (chosen) { chosen[0] = g->variant; chosen[1] = g->band; chosen[2] = (int32_t)cands.size(); }
+  return CHEMORA_OK;
+}
+
+int chemora_set_monitor(chemora_grid_t g, int enable) {
+  if (int rc = check_grid(g)) return rc;
+  if (enable && g->desc.system != CHEMORA_SYS_WAVE)
+    return fail(CHEMORA_E_UNSUPPORTED, "the fused energy monitor is defined for the wave system");
+  g->monitor = enable != 0;
+  return CHEMORA_OK;
+}
+
+int chemora_read_monitor(chemora_grid_t g, double* out, int32_t max, int32_t* count, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!count || (max > 0 && !out)) return fail(CHEMORA_E_INVALID, "bad output buffer");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t avail = g->mon_written - g->mon_read;
+  if (avail > (uint64_t)kMonHist)
+    return fail(CHEMORA_E_INVALID, "monitor ring overflowed: read at least every 1024 steps");
+  const int32_t n = (int32_t)(avail < (uint64_t)max ? avail : (uint64_t)(max > 0 ? max : 0));
+  std::vector<double> ring(kMonHist);
+  CUDA_TRY(cudaMemcpy(ring.data(), g->mon_hist, sizeof(double) * kMonHist, cudaMemcpyDeviceToHost));
+  for (int32_t i = 0; i < n; ++i) out[i] = ring[(g->mon_read + i) % kMonHist];
+  g->mon_read += n;
+  *count = n;
+  return read_nan_flag(g, st);
 }
 
 int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t nsteps, void* stream) {

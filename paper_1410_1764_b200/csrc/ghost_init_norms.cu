@@ -254,3 +254,29 @@ cudaError_t norms_partial(const Layout& L, const double* set, int system, double
 }
 
 }  // namespace chemora
+
+// ------------------------------------------------------------------ fused energy monitor
+// NEXT-3: the stage-4 kernel leaves one partial of
+// sum 1/2 (rho^2 + v.v) per CTA (Fig. 1 "Energy"); one CTA sums them in a
+// fixed order (strided per thread, then a fixed tree), so the result is deterministic.
+namespace chemora {
+namespace {
+__global__ void __launch_bounds__(1024) monitor_reduce_kernel(const double* p, int64_t n, double vol, double* out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int64_t t = threadIdx.x; t < n; t += 1024) s += p[t];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = vol * sh[0];
+}
+}  // namespace
+
+cudaError_t monitor_reduce(const double* partials, int64_t n, double vol, double* out, cudaStream_t st) {
+  monitor_reduce_kernel<<<1, 1024, 0, st>>>(partials, n, vol, out);
+  return cudaGetLastError();
+}
+}  // namespace chemora

@@ -37,6 +37,7 @@ struct StageLaunch {
   int k_begin, k_end;    // local z-plane range [k_begin, k_end)
   int variant;           // kernel variant (0 = default fast, 1 = simple reference kernel)
   int band;              // wave simple-kernel CTA band order (-1 auto, 0 plain 3-D order)
+  double* mon_partials;  // NEXT-3 fused energy monitor: per-CTA partials of stage 4 (or null)
 };
 
 // Wave (Eq. 1) -------------------------------------------------------------------------
@@ -63,6 +64,9 @@ struct InitArgs {
   double kp[4];      // kind params
 };
 cudaError_t init_interior(const Layout& L, double* set, const InitArgs& a, cudaStream_t st);
+
+// Fused energy monitor: sum n partials in fixed order, write vol * sum to *out.
+cudaError_t monitor_reduce(const double* partials, int64_t n, double vol, double* out, cudaStream_t st);
 
 // Norm partials of set y: out_dev[len] (deterministic), len = 3 n_gf (+1 wave).
 cudaError_t norms_partial(const Layout& L, const double* set, int system, double* scratch,

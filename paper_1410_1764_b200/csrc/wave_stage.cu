@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, doubl
   const int i = bx * blockDim.x + threadIdx.x;
   const int j = by * blockDim.y + threadIdx.y;
   const int k = a.k_begin + bz * blockDim.z + threadIdx.z;
-  if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
+  const bool mon = STAGE == 4 && a.mon_partials != nullptr;
+  double e = 0.0;  // NEXT-3: energy density of the new state, reduced per CTA
+  if (i < L.nx && j < L.ny && k < a.k_end) {
   const int64_t c = L.idx(i, j, k);
   const int64_t gfs = L.gfs;
   const double* in = STAGE == 0 ? a.s.y : (STAGE == 1 ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b)));
@@ -104,9 +106,27 @@ __global__ void __launch_bounds__(256) wave_simple(StageLaunch a, WaveK K, doubl
     out[f * gfs + c] = v;
     if (nf) store_images(out + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
     if (STAGE == 4) check_finite(a.nan_flag, code0 + f, v);
+    if (STAGE == 4 && f >= 1) e = fma(0.5 * v, v, e);  // eps = 1/2 (rho^2 + v.v), Fig. 1
   };
   auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
   wave_update<STAGE>(K, S, kk, Y, Qv, yu, qu, put, putq);
+  }
+  if (mon) {
+    // deterministic CTA reduction (fixed shuffle tree, then warps in order)
+    __shared__ double wsum[32];
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+    if ((tid & 31) == 0) wsum[tid >> 5] = e;
+    __syncthreads();
+    if (tid == 0) {
+      const int nw = (blockDim.x * blockDim.y * blockDim.z) >> 5;
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += wsum[w];
+      const int ntx = (int)((L.nx + 31) >> 5), nty = (int)((L.ny + blockDim.y - 1) / blockDim.y);
+      a.mon_partials[((int64_t)bz * nty + by) * ntx + bx] = s;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ z-march kernel
@@ -613,8 +633,10 @@ cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStr
   const WaveK K = make_k(a);
   // variant 0 (default) and 1: one thread per point (0: banded CTA order, 1: plain order);
   // 2: register-queue z-march; 3: TMA z-march (W <= 2).  RHS-only uses the simple kernel.
-  if (a.variant == 4 && W <= 2 && stage >= 1) return wave_tma_stage(a, stage, st);
-  if (a.variant == 5) {
+  // the fused energy monitor (NEXT-3) lives in the one-thread-per-point stage-4 kernel
+  const bool mon = stage == 4 && a.mon_partials != nullptr;
+  if (a.variant == 4 && W <= 2 && stage >= 1 && !mon) return wave_tma_stage(a, stage, st);
+  if (a.variant == 5 && !mon) {
     switch (stage) {
       case 1: return launch_brick<1, W>(a, K, st);
       case 2: return launch_brick<2, W>(a, K, st);
@@ -622,7 +644,7 @@ cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStr
       case 4: return launch_brick<4, W>(a, K, st);
     }
   }
-  if (a.variant == 3 && W == 2) {
+  if (a.variant == 3 && W == 2 && !mon) {
 
 
     switch (stage) {
@@ -632,7 +654,7 @@ cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStr
       case 4: return launch_tma<4, W>(a, K, st);
     }
   }
-  if (a.variant == 2) {
+  if (a.variant == 2 && !mon) {
     switch (stage) {
       case 1: return launch_zmarch<1, W>(a, K, st);
       case 2: return launch_zmarch<2, W>(a, K, st);

@@ -85,6 +85,15 @@ class Grid:
     def set_kernel_variant(self, v):
         C.chemora_set_kernel_variant(self.handle, v)
 
+    def set_monitor(self, enable=True):
+        C.chemora_set_monitor(self.handle, enable)
+
+    def read_monitor(self, max_steps=1024):
+        return C.chemora_read_monitor(self.handle, max_steps, self.stream)
+
+    def autotune(self, trials=3):
+        return C.chemora_autotune(self.handle, trials, self.stream)
+
     def close(self):
         if getattr(self, "handle", None) is not None:
             C.chemora_grid_destroy(self.handle)

@@ -1,0 +1,91 @@
+"""GPU tests of the SURVEY.md §8(f) NEXT rows built this round: the fused energy monitor
+(NEXT-3, Fig. 1 "Energy") and the model-driven tiling choice (NEXT-4,
+PAPER.md:419-422, 578-582).  NEXT-1 (fd order) is in test_gpu_wave.py, NEXT-2 (fission)
+in test_gpu_bssn.py / bench."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import chemora_inputs as ci
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _mods():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1410_1764_b200 as P
+    from paper_1410_1764_b200 import capi as C
+    return P, C
+
+
+@pytest.mark.parametrize("n", [(32, 32, 32), (70, 45, 33)])
+def test_fused_energy_monitor_matches_oracle(n):
+    """Energy of the state after every step, reduced inside the stage-4 kernel, equals the
+    oracle's energy of the oracle's state (1e-12) and the stand-alone norm (1e-13);
+    the state itself is bitwise unchanged by monitoring."""
+    P, C = _mods()
+    h = tuple(2 * math.pi / v for v in n)
+    dt = 0.25 * min(h)
+    y0 = ci.noise(n, 5, seed=21)
+    g = P.Grid(C.SYS_WAVE, n, h)
+    g.set_initial(C.INIT_HOST, y0)
+    g.set_monitor(True)
+    g.rk4_step(dt, 4)
+    e = g.read_monitor()
+    assert len(e) == 4
+    y = y0
+    for s in range(4):
+        y = oracle.rk4(oracle.WAVE, y, h, dt, 1)
+        assert e[s] == pytest.approx(oracle.norms(oracle.WAVE, y, h)[-1], rel=1e-12)
+    assert e[-1] == pytest.approx(g.norms()[-1], rel=1e-13)
+    assert np.all(np.diff(e) <= 1e-15 * e[0])  # RK4 energy is non-increasing
+    ref = P.Grid(C.SYS_WAVE, n, h)
+    ref.set_initial(C.INIT_HOST, y0)
+    ref.rk4_step(dt, 4)
+    assert np.array_equal(ref.get_state(), g.get_state())
+    # reading again returns nothing new; determinism across runs
+    assert len(g.read_monitor()) == 0
+    g.set_initial(C.INIT_HOST, y0)
+    g.rk4_step(dt, 4)
+    assert np.array_equal(g.read_monitor(), e)
+
+
+def test_monitor_rejects_bssn():
+    P, C = _mods()
+    g = P.Grid(C.SYS_BSSN, (16, 16, 16), (1 / 16,) * 3)
+    with pytest.raises(C.ChemoraError):
+        g.set_monitor(True)
+
+
+@pytest.mark.parametrize("system", ["wave", "bssn"])
+def test_autotune_keeps_state_and_parity(system):
+    """The autotuner times stage-1 launches with dt = 0 (state untouched) and keeps the
+    fastest candidate; stepping afterwards still matches the oracle."""
+    P, C = _mods()
+    if system == "wave":
+        n = (160, 96, 64)
+        h = tuple(2 * math.pi / v for v in n)
+        y0 = ci.noise(n, 5, seed=3)
+        g = P.Grid(C.SYS_WAVE, n, h)
+        sysid, params = oracle.WAVE, None
+    else:
+        n = (24, 24, 24)
+        h = tuple(1.0 / v for v in n)
+        y0 = ci.mink_pert(n, h, 1410)
+        g = P.Grid(C.SYS_BSSN, n, h)
+        sysid, params = oracle.BSSN, oracle.default_bssn_params()
+    g.set_initial(C.INIT_HOST, y0)
+    res = g.autotune(trials=2)
+    assert res["candidates"] >= 2 and len(res["ms"]) == res["candidates"]
+    assert np.array_equal(g.get_state(), y0)
+    dt = 0.25 * min(h)
+    g.rk4_step(dt, 2)
+    ref = oracle.rk4(sysid, y0, h, dt, 2, params)
+    err = max(np.abs(g.get_state()[f] - ref[f]).max() / max(np.abs(ref[f]).max(), 1e-6) for f in range(len(y0)))
+    assert err <= 1e-10
