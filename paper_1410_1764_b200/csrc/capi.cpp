@@ -66,6 +66,7 @@ struct chemora_grid_s {
   unsigned long long* lo_flag;  // where WE signal the lower neighbour (its flags[1])
   unsigned long long* hi_flag;  // where WE signal the upper neighbour (its flags[0])
   bool ipc;                     // neighbours are other processes (signal through flags)
+  int cur;                      // 1: the state lives in set B (rotated by fused steps)
   std::vector<void*> opened;    // IPC mappings to close
   int variant;
   int band;                     // wave CTA band order (-1 auto; CHEMORA_WAVE_BAND)
@@ -115,6 +116,13 @@ int validate(const chemora_grid_desc* d) {
     return fail(CHEMORA_E_SHAPE, "extent[2] must be divisible by nranks");
   if (d->extent[2] / d->nranks < 2 * d->ghost)
     return fail(CHEMORA_E_SHAPE, "local slab must have >= 2*ghost planes");
+  {
+    // the storage ghost width (>= 4 for 4th-order wave grids, see layout_of) must also fit
+    const int gs = (d->system == CHEMORA_SYS_WAVE && (d->fd_order == 0 || d->fd_order == 4) && d->ghost < 4)
+                       ? 4 : d->ghost;
+    if (d->extent[0] < 2 * gs || d->extent[1] < 2 * gs || d->extent[2] / d->nranks < 2 * gs)
+      return fail(CHEMORA_E_SHAPE, "4th-order wave grids need >= 8 points per axis (and per slab)");
+  }
   if (d->n_params < 0 || (d->n_params > 0 && !d->params) || d->n_params > kParams)
     return fail(CHEMORA_E_INVALID, "bad params");
   return CHEMORA_OK;
@@ -159,7 +167,12 @@ WsPlan plan_ws(const Layout& L, int system) {
 }
 
 Layout layout_of(const chemora_grid_desc& d) {
-  return make_layout(d.extent[0], d.extent[1], d.extent[2] / d.nranks, d.ghost, d.n_gf);
+  // storage ghost width: the temporally blocked wave kernels (wave_fused.cu) read their
+  // inputs with a halo of two stacked 4th-order stencils, so 4th-order wave grids keep at
+  // least 4 ghost layers in HBM; the API's ghost width (desc.ghost) is unchanged.
+  int gs = d.ghost;
+  if (d.system == CHEMORA_SYS_WAVE && (d.fd_order == 0 || d.fd_order == 4) && gs < 4) gs = 4;
+  return make_layout(d.extent[0], d.extent[1], d.extent[2] / d.nranks, gs, d.n_gf);
 }
 
 SetPtrs sets_at(char* ws, const Layout& L) {
@@ -265,6 +278,21 @@ cudaError_t launch_stage(chemora_grid_t g, const StageLaunch& a, int stage, cuda
   return g->desc.system == CHEMORA_SYS_WAVE ? wave_stage(a, stage, st) : bssn_stage(a, stage, st);
 }
 
+// Temporally blocked wave step (wave_fused.cu): two kernels per step, the new state lands
+// in the scratch set, which then becomes the state set.
+constexpr int kVariantFused = 6;
+bool use_fused(chemora_grid_t g) {
+  const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
+  return g->desc.system == CHEMORA_SYS_WAVE && g->variant == kVariantFused && order == 4 && !g->monitor &&
+         g->L.g >= 4;
+}
+void swap_state(chemora_grid_t g) {
+  std::swap(g->sets.y, g->sets.b);
+  std::swap(g->lo.y, g->lo.b);
+  std::swap(g->hi.y, g->hi.b);
+  g->cur ^= 1;
+}
+
 int read_nan_flag(chemora_grid_t g, cudaStream_t st) {
   unsigned long long flag = 0;
   CUDA_TRY(cudaMemcpyAsync(&flag, g->nan_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
@@ -279,14 +307,14 @@ int read_nan_flag(chemora_grid_t g, cudaStream_t st) {
 
 cudaMemcpy3DParms copy_params(chemora_grid_t g, int f, double* host, bool to_device, bool padded) {
   const Layout& L = g->L;
-  const int gh = L.g;
+  const int gh = g->desc.ghost;  // the API's ghost width (storage may keep more, L.g)
   cudaMemcpy3DParms p;
   memset(&p, 0, sizeof(p));
   const int64_t wx = padded ? L.nx + 2 * gh : L.nx;
-  const int64_t wy = padded ? L.py : L.ny;
-  const int64_t wz = padded ? L.pz : L.nz;
+  const int64_t wy = padded ? L.ny + 2 * gh : L.ny;
+  const int64_t wz = padded ? L.nz + 2 * gh : L.nz;
   double* dbase = g->sets.y + (size_t)f * L.gfs;  // interior origin
-  double* dstart = padded ? dbase - L.c0 + (kXOff - gh) : dbase;
+  double* dstart = padded ? dbase + L.idx(-gh, -gh, -gh) : dbase;
   // device pitched pointer: rows of px doubles, py rows per plane
   cudaPitchedPtr dev = make_cudaPitchedPtr(dstart, L.px * sizeof(double), wx * sizeof(double), L.py);
   double* hbase = host + (size_t)f * wx * wy * wz;
@@ -369,6 +397,7 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->lo_flag = g->flags + 1;
   g->hi_flag = g->flags;
   g->ipc = false;
+  g->cur = 0;
   g->variant = 0;
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
@@ -522,6 +551,19 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
   cudaStream_t st = as_stream(stream);
   const bool mon = g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0;
   const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
+  if (use_fused(g)) {
+    for (int n = 0; n < nsteps; ++n) {
+      StageLaunch a = stage_args(g, dt);
+      for (int pair = 0; pair < 2; ++pair) {
+        if (int rc = phase_wait(g, st)) return rc;
+        CUDA_TRY(wave_fused_pair(a, pair, st));
+        if (int rc = phase_signal(g, st)) return rc;
+      }
+      swap_state(g);
+      g->step += 1;
+    }
+    return CHEMORA_OK;
+  }
   for (int n = 0; n < nsteps; ++n) {
     StageLaunch a = stage_args(g, dt);
     for (int s = 1; s <= 4; ++s) {
@@ -630,12 +672,23 @@ int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t 
   if (nsteps < 0 || !std::isfinite(dt)) return fail(CHEMORA_E_INVALID, "bad dt or nsteps");
   DeviceGuard dg(grids[0]->desc.device);
   cudaStream_t st = as_stream(stream);
+  bool fused = true;
+  for (int r = 0; r < n; ++r) fused = fused && use_fused(grids[r]);
   for (int step = 0; step < nsteps; ++step) {
-    for (int s = 1; s <= 4; ++s)
-      for (int r = 0; r < n; ++r) {
-        StageLaunch a = stage_args(grids[r], dt);
-        CUDA_TRY(launch_stage(grids[r], a, s, st));
-      }
+    if (fused) {
+      for (int pair = 0; pair < 2; ++pair)
+        for (int r = 0; r < n; ++r) {
+          StageLaunch a = stage_args(grids[r], dt);
+          CUDA_TRY(wave_fused_pair(a, pair, st));
+        }
+      for (int r = 0; r < n; ++r) swap_state(grids[r]);
+    } else {
+      for (int s = 1; s <= 4; ++s)
+        for (int r = 0; r < n; ++r) {
+          StageLaunch a = stage_args(grids[r], dt);
+          CUDA_TRY(launch_stage(grids[r], a, s, st));
+        }
+    }
     for (int r = 0; r < n; ++r) grids[r]->step += 1;
   }
   return CHEMORA_OK;
@@ -774,7 +827,17 @@ int chemora_grid_connect_ipc(chemora_grid_t g, const void* rlo, const void* rhi)
   if (n == 2) bhi = blo;  // both faces go to the same peer
   else if (int rc = open(hi, &bhi)) return rc;
   g->lo = sets_at(blo, g->L);
+  if (g->cur) {  // state/scratch sets already rotated by fused steps (neighbours in lockstep)
+    SetPtrs t = sets_at(blo, g->L);
+    g->lo.y = t.b;
+    g->lo.b = t.y;
+  }
   g->hi = sets_at(bhi, g->L);
+  if (g->cur) {
+    SetPtrs t = sets_at(bhi, g->L);
+    g->hi.y = t.b;
+    g->hi.b = t.y;
+  }
   // we signal the lower neighbour in its flags[1] ("from hi") and the upper in flags[0]
   g->lo_flag = reinterpret_cast<unsigned long long*>(blo + P.flags) + 2;
   g->hi_flag = reinterpret_cast<unsigned long long*>(bhi + P.flags) + 1;

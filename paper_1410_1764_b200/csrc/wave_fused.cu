@@ -1,0 +1,426 @@
+// wave_fused.cu -- temporally blocked RK4 for the wave equation (Eq. 1):
+// two stage pairs per step instead of four stage kernels, so the intermediate states Y2 and
+// Y4 never travel through HBM.
+//
+//   kernel A (stages 1+2): reads y;             Y2 = y + dt/2 k1(y) on the tile + stencil halo,
+//                          kept in shared memory; writes Q = (y + Y2)/3 + dt/3 k2(Y2),
+//                          C = y + dt/2 k2(Y2), Q.u = dt/6 y.rho + dt/3 Y2.rho.
+//   kernel B (stages 3+4): reads C, y, Q;       Y4 = y + dt k3(C) on the tile + halo in SMEM;
+//                          writes y' = Q + Y4/3 + dt/6 k4(Y4), y'.u = y.u + Q.u + dt/6 Y4.rho
+//                          into the scratch set (the caller swaps the state and scratch sets).
+// HBM traffic per point-update: A 4 reads + 9 writes, B 14 reads + 5 writes = 32 GF passes
+// = 256 B, against 54 passes = 432 B for one kernel per stage.
+// This is the kernel fusion of PAPER.md:537-547 carried across RK stages.
+//
+// Structure (both kernels): persistent, one CTA per SM walks (tile 32x8, z chunk) items; a
+// producer thread streams the inputs with TMA into mbarrier rings; eight consumer warps
+// first compute the intermediate state on the tile extended by the stencil radius for plane
+// p = k + 2 (z-derivatives of the inputs from the ring's neighbouring planes), then the
+// second stage at plane k from the intermediate-state ring.  The per-point operation
+// sequence is exactly that of the one-kernel-per-stage path (bit-identical results; no FMA
+// contraction in this file).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdlib>
+#include "grid.hpp"
+#include "kernels.hpp"
+#include "device_common.cuh"
+#include "tma.cuh"
+#include "wave_common.cuh"
+
+namespace chemora {
+namespace {
+using namespace wave;
+
+constexpr int TX = 32, TY = 8, NCW = 8, NT = 32 * (NCW + 1);
+constexpr int W = 2;   // 4th-order stencils (fd_order 4 only)
+constexpr int H = 4;   // input halo: two stacked radius-2 stencils
+constexpr int r128(int b) { return (b + 127) / 128 * 128; }
+
+// input box geometries (x extent, y extent, x origin offset, y origin offset)
+constexpr int BR_X = TX + 2 * H, BR_Y = TY + 2 * H;      // rho   (40 x 16), origin (-4,-4)
+constexpr int B3_X = TX + 2 * W, B3_Y = TY + 2 * W;      // v3    (36 x 12), origin (-2,-2)
+constexpr int B1_X = TX + 2 * H, B1_Y = TY + 2 * W;      // v1    (40 x 12), origin (-4,-2)
+constexpr int B2_X = TX + 2 * W, B2_Y = TY + 2 * H;      // v2    (36 x 16), origin (-2,-4)
+// intermediate-state geometries
+constexpr int IR_X = TX + 2 * W, IR_Y = TY + 2 * W;      // rho   (36 x 12), origin (-2,-2)
+constexpr int I1_X = TX + 2 * W, I1_Y = TY;              // v1    (36 x 8),  origin (-2, 0)
+constexpr int I2_X = TX, I2_Y = TY + 2 * W;              // v2    (32 x 12), origin ( 0,-2)
+constexpr int I3_X = TX, I3_Y = TY;                      // v3    (32 x 8)
+// pointwise boxes of kernel B (y on the intermediate geometries, Q and y.u centres)
+constexpr int C1 = TX * TY;
+
+constexpr int ZR_B = r128(BR_X * BR_Y * 8), Z3_B = r128(B3_X * B3_Y * 8);
+constexpr int ZSLOT = ZR_B + Z3_B;
+constexpr uint32_t ZBYTES = (BR_X * BR_Y + B3_X * B3_Y) * 8;
+constexpr int P1_B = r128(B1_X * B1_Y * 8), P2_B = r128(B2_X * B2_Y * 8);
+constexpr int PY_R = r128(IR_X * IR_Y * 8), PY_1 = r128(I1_X * I1_Y * 8), PY_2 = r128(I2_X * I2_Y * 8),
+              PY_3 = r128(I3_X * I3_Y * 8);
+constexpr int IZ_B = r128(IR_X * IR_Y * 8) + r128(I3_X * I3_Y * 8);  // intermediate z ring slot
+constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermediate p ring slot
+constexpr int RZ = 7, RI_Z = 5, RI_P = 3;
+
+template <bool B> struct Geo {
+  static constexpr int RP = B ? 4 : 5;
+  static constexpr int RQ = B ? 3 : 0;
+  static constexpr int PSLOT = P1_B + P2_B + (B ? PY_R + PY_1 + PY_2 + PY_3 : 0);
+  static constexpr uint32_t PBYTES =
+      (B1_X * B1_Y + B2_X * B2_Y + (B ? IR_X * IR_Y + I1_X * I1_Y + I2_X * I2_Y + I3_X * I3_Y : 0)) * 8;
+  static constexpr int QSLOT = B ? r128(6 * C1 * 8) : 0;  // Q (u, rho, v1..3) + y.u
+  static constexpr uint32_t QBYTES = B ? 6 * C1 * 8 : 0;
+  static constexpr int OFF_P = RZ * ZSLOT;
+  static constexpr int OFF_Q = OFF_P + RP * PSLOT;
+  static constexpr int OFF_IZ = OFF_Q + RQ * QSLOT;
+  static constexpr int OFF_IP = OFF_IZ + RI_Z * IZ_B;
+  static constexpr int OFF_BAR = OFF_IP + RI_P * IP_B;
+  static constexpr int NBAR = 2 * RZ + 2 * RP + 2 * RQ;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8;
+};
+
+struct FMaps {
+  CUtensorMap rho, v3, v1, v2;       // stencil input set (A: y, B: C)
+  CUtensorMap yr, y1, y2, y3;        // B: y on the intermediate geometries
+  CUtensorMap q5, yu;                // B: Q centres (5 GFs) and y.u centre
+};
+
+// shared-memory centered D1 (no 1/h), same operation order as wave::d1
+__device__ __forceinline__ double d1s_(const double* f, int c, int s) {
+  double acc = 0.0;
+#pragma unroll
+  for (int q = W; q >= 1; --q) acc = fma(D1W<W>::c(q), f[c + q * s] - f[c - q * s], acc);
+  return acc;
+}
+
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"r"(32 * NCW) : "memory"); }
+
+template <bool B>
+__global__ void __launch_bounds__(NT, 1)
+    wave_fused(const __grid_constant__ FMaps M, StageLaunch a, WaveK K, int kchunk, int ntx, int nty, int nitems) {
+  using G = Geo<B>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  uint64_t* zfull = bars;
+  uint64_t* zempty = zfull + RZ;
+  uint64_t* pfull = zempty + RZ;
+  uint64_t* pempty = pfull + G::RP;
+  uint64_t* qfull = pempty + G::RP;
+  uint64_t* qempty = qfull + G::RQ;
+  const Layout& L = a.L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, NCW); }
+    for (int s = 0; s < G::RP; ++s) { mbar_init(pfull + s, 1); mbar_init(pempty + s, NCW); }
+    for (int s = 0; s < G::RQ; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, NCW); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int g = L.g;
+  const int nkall = a.k_end - a.k_begin;
+
+  if (warp == NCW) {  // ------------------------------------------------------ producer
+    if (lane != 0) return;
+    uint32_t nz = 0, np = 0, nq = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
+      const int i0 = bx * TX, j0 = by * TY;
+      const int kb = a.k_begin + ch * kchunk;
+      const int nk = min(kchunk, a.k_begin + nkall - kb);
+      const int xo = kXOff + i0, yo = g + j0;
+      auto loadZ = [&](int plane) {
+        const uint32_t s = nz % RZ, n = nz / RZ;
+        if (n > 0) mbar_wait(zempty + s, (n - 1) & 1);
+        unsigned char* d = smem + s * ZSLOT;
+        mbar_arrive_expect_tx(zfull + s, ZBYTES);
+        tma_load_4d(d, &M.rho, zfull + s, xo - H, yo - H, g + plane, GRHO);
+        tma_load_4d(d + ZR_B, &M.v3, zfull + s, xo - W, yo - W, g + plane, GV3);
+        ++nz;
+      };
+      auto loadP = [&](int plane) {
+        const uint32_t s = np % G::RP, n = np / G::RP;
+        if (n > 0) mbar_wait(pempty + s, (n - 1) & 1);
+        unsigned char* d = smem + G::OFF_P + s * G::PSLOT;
+        uint64_t* bar = pfull + s;
+        mbar_arrive_expect_tx(bar, G::PBYTES);
+        tma_load_4d(d, &M.v1, bar, xo - H, yo - W, g + plane, GV1);
+        tma_load_4d(d + P1_B, &M.v2, bar, xo - W, yo - H, g + plane, GV2);
+        if (B) {
+          unsigned char* e = d + P1_B + P2_B;
+          tma_load_4d(e, &M.yr, bar, xo - W, yo - W, g + plane, GRHO);
+          tma_load_4d(e + PY_R, &M.y1, bar, xo - W, yo, g + plane, GV1);
+          tma_load_4d(e + PY_R + PY_1, &M.y2, bar, xo, yo - W, g + plane, GV2);
+          tma_load_4d(e + PY_R + PY_1 + PY_2, &M.y3, bar, xo, yo, g + plane, GV3);
+        }
+        ++np;
+      };
+      auto loadQ = [&](int plane) {
+        const uint32_t s = nq % G::RQ, n = nq / G::RQ;
+        if (n > 0) mbar_wait(qempty + s, (n - 1) & 1);
+        unsigned char* d = smem + G::OFF_Q + s * G::QSLOT;
+        mbar_arrive_expect_tx(qfull + s, G::QBYTES);
+        tma_load_4d(d, &M.q5, qfull + s, xo, yo, g + plane, GU);
+        tma_load_4d(d + 5 * C1 * 8, &M.yu, qfull + s, xo, yo, g + plane, GU);
+        ++nq;
+      };
+      // intermediate planes p = kb-2 .. kb+nk+1 need input planes p-2 .. p+2
+      for (int pl = kb - 4; pl < kb; ++pl) loadZ(pl);
+      for (int j = 0; j < nk + 4; ++j) {
+        const int p = kb - 2 + j;
+        loadZ(p + 2);
+        loadP(p);
+        if (B && p - 2 >= kb) loadQ(p - 2);
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------------------- consumers
+  const int tid = threadIdx.x;
+  const int64_t gfs = L.gfs;
+  uint32_t nz = 0, np = 0, nq = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
+    const int i0 = bx * TX, j0 = by * TY;
+    const int kb = a.k_begin + ch * kchunk;
+    const int nk = min(kchunk, a.k_begin + nkall - kb);
+    const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
+    for (int q = 0; q < 4; ++q) mbar_wait(zfull + (z0 + q) % RZ, ((z0 + q) / RZ) & 1);
+    const int ti = lane, tj = warp;   // this thread's point in the tile (second stage)
+    const int i = i0 + ti, j = j0 + tj;
+    const bool live = i < L.nx && j < L.ny;
+#pragma unroll 1
+    for (int jj = 0; jj < nk + 4; ++jj) {
+      const int p = kb - 2 + jj;
+      const uint32_t zi = z0 + jj + 4;  // ring index of input plane p + 2
+      mbar_wait(zfull + zi % RZ, (zi / RZ) & 1);
+      const uint32_t pi = p0 + jj;      // ring index of P plane p
+      mbar_wait(pfull + pi % G::RP, (pi / G::RP) & 1);
+      // input plane pointers p-2 .. p+2
+      const double* zR[5];
+      const double* z3[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const unsigned char* sl = smem + ((z0 + jj + q) % RZ) * ZSLOT;
+        zR[q] = reinterpret_cast<const double*>(sl);
+        z3[q] = reinterpret_cast<const double*>(sl + ZR_B);
+      }
+      const unsigned char* ps = smem + G::OFF_P + (pi % G::RP) * G::PSLOT;
+      const double* s1 = reinterpret_cast<const double*>(ps);
+      const double* s2 = reinterpret_cast<const double*>(ps + P1_B);
+      const double* sy = reinterpret_cast<const double*>(ps + P1_B + P2_B);  // B only
+      // intermediate slots for plane p
+      unsigned char* iz = smem + G::OFF_IZ + ((jj) % RI_Z) * IZ_B;
+      unsigned char* ip = smem + G::OFF_IP + ((jj) % RI_P) * IP_B;
+      double* IR = reinterpret_cast<double*>(iz);
+      double* I3 = reinterpret_cast<double*>(iz + r128(IR_X * IR_Y * 8));
+      double* I1 = reinterpret_cast<double*>(ip);
+      double* I2 = reinterpret_cast<double*>(ip + r128(I1_X * I1_Y * 8));
+      cbar();  // everyone is done with the intermediate slots being overwritten
+      // ---- intermediate state at plane p: Y2 = y + dt/2 k1(y) (A) or Y4 = y + dt k3(C) (B)
+      const double cdt = B ? K.dt : K.dt2;
+      for (int e = tid; e < IR_X * IR_Y; e += 32 * NCW) {   // rho on (36 x 12)
+        const int x = e % IR_X, y = e / IR_X;                 // tile coords x-2, y-2
+        const int c1 = y * B1_X + x + 2;            // v1 box: origin (-4,-2) -> (x-2)+4, (y-2)+2
+        const int c2 = (y + 2) * B2_X + x;          // v2 box: origin (-2,-4) -> (x-2)+2, (y-2)+4
+        const int c3 = y * B3_X + x;                // v3 box: origin (-2,-2)
+        const double dv1 = d1s_(s1, c1, 1) * K.ih[0];
+        const double dv2 = d1s_(s2, c2, B2_X) * K.ih[1];
+        double dv3 = 0.0;
+#pragma unroll
+        for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][c3] - z3[2 - q][c3], dv3);
+        dv3 = dv3 * K.ih[2];
+        const double k = dv1 + dv2 + dv3;
+        const double base = B ? sy[e] : zR[2][(y + 2) * BR_X + x + 2];
+        IR[e] = fma(cdt, k, base);
+      }
+      for (int e = tid; e < I1_X * I1_Y; e += 32 * NCW) {   // v1 on (36 x 8)
+        const int x = e % I1_X, y = e / I1_X;                 // tile coords x-2, y
+        const int cr = (y + 4) * BR_X + x + 2;                // rho box origin (-4,-4)
+        const double k = d1s_(zR[2], cr, 1) * K.ih[0];
+        const double base = B ? sy[PY_R / 8 + e] : s1[(y + 2) * B1_X + x + 2];
+        I1[e] = fma(cdt, k, base);
+      }
+      for (int e = tid; e < I2_X * I2_Y; e += 32 * NCW) {   // v2 on (32 x 12)
+        const int x = e % I2_X, y = e / I2_X;                 // tile coords x, y-2
+        const int cr = (y + 2) * BR_X + x + 4;
+        const double k = d1s_(zR[2], cr, BR_X) * K.ih[1];
+        const double base = B ? sy[(PY_R + PY_1) / 8 + e] : s2[(y + 2) * B2_X + x + 2];
+        I2[e] = fma(cdt, k, base);
+      }
+      for (int e = tid; e < I3_X * I3_Y; e += 32 * NCW) {   // v3 on (32 x 8)
+        const int x = e % I3_X, y = e / I3_X;
+        const int cr = (y + 4) * BR_X + x + 4;
+        double dzr = 0.0;
+#pragma unroll
+        for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[2 + q][cr] - zR[2 - q][cr], dzr);
+        const double k = dzr * K.ih[2];
+        const double base = B ? sy[(PY_R + PY_1 + PY_2) / 8 + e] : z3[2][(y + 2) * B3_X + x + 2];
+        I3[e] = fma(cdt, k, base);
+      }
+      cbar();  // the intermediate plane p is complete
+      // ---- second stage at plane k = p - 2
+      const int k = p - 2;
+      if (k >= kb) {
+        const int ki = jj - 2;  // intermediate index of plane k
+        const double* iR[5];
+        const double* i3[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const unsigned char* sl = smem + G::OFF_IZ + ((ki - 2 + q + RI_Z) % RI_Z) * IZ_B;
+          iR[q] = reinterpret_cast<const double*>(sl);
+          i3[q] = reinterpret_cast<const double*>(sl + r128(IR_X * IR_Y * 8));
+        }
+        const unsigned char* ipk = smem + G::OFF_IP + (ki % RI_P) * IP_B;
+        const double* i1 = reinterpret_cast<const double*>(ipk);
+        const double* i2 = reinterpret_cast<const double*>(ipk + r128(I1_X * I1_Y * 8));
+        const int cr = (tj + 2) * IR_X + ti + 2, c1 = tj * I1_X + ti + 2, c2 = (tj + 2) * I2_X + ti,
+                  c3 = tj * I3_X + ti;
+        double S[5], kk[5];
+        S[GRHO] = iR[2][cr];
+        S[GV1] = i1[c1];
+        S[GV2] = i2[c2];
+        S[GV3] = i3[2][c3];
+        double dzr = 0.0, dv3 = 0.0;
+#pragma unroll
+        for (int q = W; q >= 1; --q) {
+          dzr = fma(D1W<W>::c(q), iR[2 + q][cr] - iR[2 - q][cr], dzr);
+          dv3 = fma(D1W<W>::c(q), i3[2 + q][c3] - i3[2 - q][c3], dv3);
+        }
+        const double dxr = d1s_(iR[2], cr, 1) * K.ih[0];
+        const double dyr = d1s_(iR[2], cr, IR_X) * K.ih[1];
+        dzr = dzr * K.ih[2];
+        const double dv1 = d1s_(i1, c1, 1) * K.ih[0];
+        const double dv2 = d1s_(i2, c2, I2_X) * K.ih[1];
+        dv3 = dv3 * K.ih[2];
+        kk[GRHO] = dv1 + dv2 + dv3;
+        kk[GV1] = dxr;
+        kk[GV2] = dyr;
+        kk[GV3] = dzr;
+        double Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
+        if (!B) {
+          // y at plane k: input ring planes k = p - 2 -> zR[0], P plane k = P ring index pi - 2
+          const unsigned char* pk = smem + G::OFF_P + ((pi - 2) % G::RP) * G::PSLOT;
+          const double* k1 = reinterpret_cast<const double*>(pk);
+          const double* k2 = reinterpret_cast<const double*>(pk + P1_B);
+          Y[GRHO] = zR[0][(tj + 4) * BR_X + ti + 4];
+          Y[GV1] = k1[(tj + 2) * B1_X + ti + 4];
+          Y[GV2] = k2[(tj + 4) * B2_X + ti + 2];
+          Y[GV3] = z3[0][(tj + 2) * B3_X + ti + 2];
+        } else {
+          const uint32_t qi = nq;
+          mbar_wait(qfull + qi % G::RQ, (qi / G::RQ) & 1);
+          const double* qs = reinterpret_cast<const double*>(smem + G::OFF_Q + (qi % G::RQ) * G::QSLOT);
+          const int cc = tj * TX + ti;
+          qu = qs[cc];
+#pragma unroll
+          for (int f = 1; f <= 4; ++f) Qv[f] = qs[f * C1 + cc];
+          yu = qs[5 * C1 + cc];
+        }
+        if (live) {
+          const int64_t c = L.idx(i, j, k);
+          const bool nf = near_face(L, i, j, k);
+          if (!B) {
+            double* outc = a.s.c;
+            const FaceDst fd = a.img[1];
+            auto put = [&](int f, double v) {
+              outc[f * gfs + c] = v;
+              if (nf) store_images(outc + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+            };
+            auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
+            wave_update<2>(K, S, kk, Y, Qv, yu, qu, put, putq);
+          } else {
+            double* outy = a.s.b;  // the new state goes to the scratch set (swapped by the caller)
+            const FaceDst fd = a.img[0];
+            const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
+            auto put = [&](int f, double v) {
+              outy[f * gfs + c] = v;
+              if (nf) store_images(outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+              check_finite(a.nan_flag, code0 + f, v);
+            };
+            auto putq = [&](int, double) {};
+            wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (B) mbar_arrive(qempty + nq % G::RQ);
+          mbar_arrive(pempty + (pi - 2) % G::RP);  // P plane k
+        }
+        if (B) ++nq;
+      } else if (jj < 2) {
+        // planes kb-2, kb-1 never reach the second stage: free their P slots now
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pempty + pi % G::RP);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(zempty + (z0 + jj) % RZ);  // input plane p - 2
+    }
+    // the last two P planes (ke, ke+1) and input planes ke .. ke+3 were only read
+    __syncwarp();
+    if (lane == 0) {
+      for (int q = 0; q < 2; ++q) mbar_arrive(pempty + (p0 + nk + 2 + q) % G::RP);
+      for (int q = 0; q < 4; ++q) mbar_arrive(zempty + (z0 + nk + 4 + q) % RZ);
+    }
+    nz = z0 + nk + 8;
+    np = p0 + nk + 4;
+  }
+}
+
+bool enc(CUtensorMap* m, const double* set, const Layout& L, unsigned bx, unsigned by, unsigned bg) {
+  return encode_set_map(m, set - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, bx, by, bg);
+}
+
+WaveK make_k(const StageLaunch& a) {
+  WaveK K;
+  for (int d = 0; d < 3; ++d) K.ih[d] = 1.0 / a.h[d];
+  K.half = 0.5; K.third = 1.0 / 3.0; K.sixth = 1.0 / 6.0;
+  K.dt = a.dt; K.dt2 = a.dt / 2.0; K.dt3 = a.dt / 3.0; K.dt6 = a.dt / 6.0;
+  return K;
+}
+
+template <bool B>
+cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
+  using G = Geo<B>;
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  const Layout& L = a.L;
+  const double* in = B ? a.s.c : a.s.y;
+  FMaps M;
+  bool ok = enc(&M.rho, in, L, BR_X, BR_Y, 1) && enc(&M.v3, in, L, B3_X, B3_Y, 1) &&
+            enc(&M.v1, in, L, B1_X, B1_Y, 1) && enc(&M.v2, in, L, B2_X, B2_Y, 1) &&
+            enc(&M.yr, a.s.y, L, IR_X, IR_Y, 1) && enc(&M.y1, a.s.y, L, I1_X, I1_Y, 1) &&
+            enc(&M.y2, a.s.y, L, I2_X, I2_Y, 1) && enc(&M.y3, a.s.y, L, I3_X, I3_Y, 1) &&
+            enc(&M.q5, a.s.q, L, TX, TY, 5) && enc(&M.yu, a.s.y, L, TX, TY, 1);
+  if (!ok) return cudaErrorInvalidValue;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(wave_fused<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
+  int nchunks = (nk + 63) / 64;
+  const int want = (8 * nsm + ntx * nty - 1) / (ntx * nty);
+  if (nchunks < want) nchunks = want;
+  int chunk = (nk + nchunks - 1) / nchunks;
+  if (chunk < 2) chunk = 2;
+  if (chunk > nk) chunk = nk;
+  nchunks = (nk + chunk - 1) / chunk;
+  const int nitems = ntx * nty * nchunks;
+  const int grid = nitems < nsm ? nitems : nsm;
+  const WaveK K = make_k(a);
+  wave_fused<B><<<grid, NT, G::SMEM, st>>>(M, a, K, chunk, ntx, nty, nitems);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t wave_fused_pair(const StageLaunch& a, int pair, cudaStream_t st) {
+  if (a.fd_order != 4) return cudaErrorInvalidValue;
+  return pair == 0 ? launch<false>(a, st) : launch<true>(a, st);
+}
+
+}  // namespace chemora
