@@ -207,6 +207,10 @@ int chemora_autotune(chemora_grid_t grid, int32_t trials, int32_t* chosen, doubl
  * 1 = one-thread-per-point reference kernel.  Results must be bitwise identical. */
 int chemora_set_kernel_variant(chemora_grid_t grid, int variant);
 
+/* Copy state set `set` (0 = y, 1 = Q, 2 = B, 3 = C, in the current rotation) padded to host
+ * [gf][Nz+2g][Ny+2g][Nx+2g].  Synchronises. */
+int chemora_debug_get_set(chemora_grid_t grid, int set, double* host_dst, void* stream);
+
 /* chemora_set_initial without the final halo exchange (ghosts left as cleared/copied). */
 int chemora_set_initial_nofill(chemora_grid_t grid, int kind, const double* host_src,
                                const double* kind_params, uint64_t seed, void* stream);

@@ -522,6 +522,17 @@ static int get_state_impl(chemora_grid_t g, double* host, void* stream, bool pad
   return read_nan_flag(g, st);
 }
 
+int chemora_debug_get_set(chemora_grid_t g, int set, double* host, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (set < 0 || set > 3 || !host) return fail(CHEMORA_E_INVALID, "bad set");
+  SetPtrs saved = g->sets;
+  double* p[4] = {g->sets.y, g->sets.q, g->sets.b, g->sets.c};
+  g->sets.y = p[set];
+  int rc = get_state_impl(g, host, stream, true);
+  g->sets = saved;
+  return rc;
+}
+
 int chemora_get_state(chemora_grid_t g, double* host, void* stream) {
   return get_state_impl(g, host, stream, false);
 }
@@ -551,10 +562,16 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
   cudaStream_t st = as_stream(stream);
   const bool mon = g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0;
   const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
+  static int dbg_stop = -1;  // CHEMORA_DEBUG_STOP=s: run only stages <= s (test hook)
+  if (dbg_stop < 0) {
+    const char* e = getenv("CHEMORA_DEBUG_STOP");
+    dbg_stop = e ? atoi(e) : 4;
+  }
   if (use_fused(g)) {
     for (int n = 0; n < nsteps; ++n) {
       StageLaunch a = stage_args(g, dt);
       for (int pair = 0; pair < 2; ++pair) {
+        if (2 * pair + 2 > dbg_stop) return CHEMORA_OK;
         if (int rc = phase_wait(g, st)) return rc;
         CUDA_TRY(wave_fused_pair(a, pair, st));
         if (int rc = phase_signal(g, st)) return rc;
@@ -567,6 +584,7 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
   for (int n = 0; n < nsteps; ++n) {
     StageLaunch a = stage_args(g, dt);
     for (int s = 1; s <= 4; ++s) {
+      if (s > dbg_stop) return CHEMORA_OK;
       if (int rc = phase_wait(g, st)) return rc;
       if (s == 4 && mon) {
         CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));

@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(NT, 1)
           mbar_wait(qfull + qi % G::RQ, (qi / G::RQ) & 1);
           const double* qs = reinterpret_cast<const double*>(smem + G::OFF_Q + (qi % G::RQ) * G::QSLOT);
           const int cc = tj * TX + ti;
-          qu = qs[cc];
+          // u carry of stage 3 (folded): Q.u += dt/3 C.rho, with C.rho at plane k from the ring
+          qu = fma(K.dt3, zR[0][(tj + 4) * BR_X + ti + 4], qs[cc]);
 #pragma unroll
           for (int f = 1; f <= 4; ++f) Qv[f] = qs[f * C1 + cc];
           yu = qs[5 * C1 + cc];
