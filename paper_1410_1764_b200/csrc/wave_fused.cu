@@ -174,8 +174,62 @@ __global__ void __launch_bounds__(NT, 1)
   }
 
   // --------------------------------------------------------------------------- consumers
+  // All shared-memory offsets below are per-thread constants (computed once); the ring
+  // slots advance by increment-and-wrap, so the per-plane loop is loads, flops and stores.
   const int tid = threadIdx.x;
   const int64_t gfs = L.gfs;
+  constexpr int NTC = 32 * NCW;
+  constexpr int IRN = IR_X * IR_Y, I1N = I1_X * I1_Y, I2N = I2_X * I2_Y, I3N = I3_X * I3_Y;
+  static_assert(IRN <= 2 * NTC && I1N <= 2 * NTC && I2N <= 2 * NTC && I3N == NTC, "tile geometry");
+  // intermediate rho elements e = tid, tid + NTC: offsets into v1/v2/v3/rho(or y) boxes
+  int rR_c1[2], rR_c2[2], rR_c3[2], rR_b[2];
+  bool rR_ok[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * NTC;
+    rR_ok[u] = e < IRN;
+    const int x = e % IR_X, y = e / IR_X;
+    rR_c1[u] = y * B1_X + x + 2;
+    rR_c2[u] = (y + 2) * B2_X + x;
+    rR_c3[u] = y * B3_X + x;
+    rR_b[u] = (y + 2) * BR_X + x + 2;
+  }
+  int r1_cr[2], r1_b[2];
+  bool r1_ok[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * NTC;
+    r1_ok[u] = e < I1N;
+    const int x = e % I1_X, y = e / I1_X;
+    r1_cr[u] = (y + 4) * BR_X + x + 2;
+    r1_b[u] = (y + 2) * B1_X + x + 2;
+  }
+  int r2_cr[2], r2_b[2];
+  bool r2_ok[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * NTC;
+    r2_ok[u] = e < I2N;
+    const int x = e % I2_X, y = e / I2_X;
+    r2_cr[u] = (y + 2) * BR_X + x + 4;
+    r2_b[u] = (y + 2) * B2_X + x + 2;
+  }
+  const int r3_cr = (tid / I3_X + 4) * BR_X + tid % I3_X + 4;
+  const int r3_b = (tid / I3_X + 2) * B3_X + tid % I3_X + 2;
+  // second stage: this thread's point (ti, tj) of the tile
+  const int ti = lane, tj = warp;
+  const int s_cr = (tj + 2) * IR_X + ti + 2, s_c1 = tj * I1_X + ti + 2, s_c2 = (tj + 2) * I2_X + ti,
+            s_c3 = tj * I3_X + ti;
+  const int y_r = (tj + 4) * BR_X + ti + 4, y_1 = (tj + 2) * B1_X + ti + 4, y_2 = (tj + 4) * B2_X + ti + 2,
+            y_3 = (tj + 2) * B3_X + ti + 2;
+  const int cc = tj * TX + ti;
+  const double cdt = B ? K.dt : K.dt2;
+  double* const sm = reinterpret_cast<double*>(smem);
+  constexpr int ZSD = ZSLOT / 8, ZR_D = ZR_B / 8, PSD = G::PSLOT / 8, P1D = P1_B / 8, P2D = P2_B / 8;
+  constexpr int IZD = IZ_B / 8, IPD = IP_B / 8, IR_D = r128(IR_X * IR_Y * 8) / 8, I1_D = r128(I1_X * I1_Y * 8) / 8;
+  constexpr int OFF_PD = G::OFF_P / 8, OFF_QD = G::OFF_Q / 8, OFF_IZD = G::OFF_IZ / 8, OFF_IPD = G::OFF_IP / 8;
+  constexpr int PYR = PY_R / 8, PY1 = PY_1 / 8, PY2 = PY_2 / 8;
+
   uint32_t nz = 0, np = 0, nq = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
@@ -184,112 +238,113 @@ __global__ void __launch_bounds__(NT, 1)
     const int nk = min(kchunk, a.k_begin + nkall - kb);
     const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
     for (int q = 0; q < 4; ++q) mbar_wait(zfull + (z0 + q) % RZ, ((z0 + q) / RZ) & 1);
-    const int ti = lane, tj = warp;   // this thread's point in the tile (second stage)
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
+    int64_t cglob = L.idx(i, j, kb);  // global offset of this thread's point at plane k
+    // ring slots: input planes p-2..p+2, P planes p and p-2, intermediate planes
+    int zsl[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) zsl[q] = (int)((z0 + q) % RZ);
+    int psl = (int)(p0 % G::RP), psl2 = 0;   // P slot of plane p, of plane p-2
+    int zph = (int)(((z0 + 4) / RZ) & 1);    // phase of the input slot zsl[4]
+    int pph = (int)((p0 / G::RP) & 1);
+    int izs[5] = {0, 0, 0, 0, 0};           // intermediate z slots of planes p-4..p
+    int ips[3] = {0, 0, 0};                 // intermediate p slots of planes p-2..p
 #pragma unroll 1
     for (int jj = 0; jj < nk + 4; ++jj) {
       const int p = kb - 2 + jj;
-      const uint32_t zi = z0 + jj + 4;  // ring index of input plane p + 2
-      mbar_wait(zfull + zi % RZ, (zi / RZ) & 1);
-      const uint32_t pi = p0 + jj;      // ring index of P plane p
-      mbar_wait(pfull + pi % G::RP, (pi / G::RP) & 1);
-      // input plane pointers p-2 .. p+2
+      // intermediate slot of plane p (jj mod 5 / mod 3), kept incrementally
+#pragma unroll
+      for (int q = 0; q < 4; ++q) izs[q] = izs[q + 1];
+      izs[4] = jj % RI_Z;
+      ips[0] = ips[1];
+      ips[1] = ips[2];
+      ips[2] = jj % RI_P;
+      mbar_wait(zfull + zsl[4], zph);
+      mbar_wait(pfull + psl, pph);
       const double* zR[5];
       const double* z3[5];
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
-        const unsigned char* sl = smem + ((z0 + jj + q) % RZ) * ZSLOT;
-        zR[q] = reinterpret_cast<const double*>(sl);
-        z3[q] = reinterpret_cast<const double*>(sl + ZR_B);
+        zR[q] = sm + zsl[q] * ZSD;
+        z3[q] = zR[q] + ZR_D;
       }
-      const unsigned char* ps = smem + G::OFF_P + (pi % G::RP) * G::PSLOT;
-      const double* s1 = reinterpret_cast<const double*>(ps);
-      const double* s2 = reinterpret_cast<const double*>(ps + P1_B);
-      const double* sy = reinterpret_cast<const double*>(ps + P1_B + P2_B);  // B only
-      // intermediate slots for plane p
-      unsigned char* iz = smem + G::OFF_IZ + ((jj) % RI_Z) * IZ_B;
-      unsigned char* ip = smem + G::OFF_IP + ((jj) % RI_P) * IP_B;
-      double* IR = reinterpret_cast<double*>(iz);
-      double* I3 = reinterpret_cast<double*>(iz + r128(IR_X * IR_Y * 8));
-      double* I1 = reinterpret_cast<double*>(ip);
-      double* I2 = reinterpret_cast<double*>(ip + r128(I1_X * I1_Y * 8));
+      const double* s1 = sm + OFF_PD + psl * PSD;
+      const double* s2 = s1 + P1D;
+      const double* sy = s2 + P2D;  // B only
+      double* IR = sm + OFF_IZD + izs[4] * IZD;
+      double* I3 = IR + IR_D;
+      double* I1 = sm + OFF_IPD + ips[2] * IPD;
+      double* I2 = I1 + I1_D;
       cbar();  // everyone is done with the intermediate slots being overwritten
       // ---- intermediate state at plane p: Y2 = y + dt/2 k1(y) (A) or Y4 = y + dt k3(C) (B)
-      const double cdt = B ? K.dt : K.dt2;
-      for (int e = tid; e < IR_X * IR_Y; e += 32 * NCW) {   // rho on (36 x 12)
-        const int x = e % IR_X, y = e / IR_X;                 // tile coords x-2, y-2
-        const int c1 = y * B1_X + x + 2;            // v1 box: origin (-4,-2) -> (x-2)+4, (y-2)+2
-        const int c2 = (y + 2) * B2_X + x;          // v2 box: origin (-2,-4) -> (x-2)+2, (y-2)+4
-        const int c3 = y * B3_X + x;                // v3 box: origin (-2,-2)
-        const double dv1 = d1s_(s1, c1, 1) * K.ih[0];
-        const double dv2 = d1s_(s2, c2, B2_X) * K.ih[1];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!rR_ok[u]) continue;
+        const double dv1 = d1s_(s1, rR_c1[u], 1) * K.ih[0];
+        const double dv2 = d1s_(s2, rR_c2[u], B2_X) * K.ih[1];
         double dv3 = 0.0;
 #pragma unroll
-        for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][c3] - z3[2 - q][c3], dv3);
+        for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][rR_c3[u]] - z3[2 - q][rR_c3[u]], dv3);
         dv3 = dv3 * K.ih[2];
         const double k = dv1 + dv2 + dv3;
-        const double base = B ? sy[e] : zR[2][(y + 2) * BR_X + x + 2];
+        const int e = tid + u * NTC;
+        const double base = B ? sy[e] : zR[2][rR_b[u]];
         IR[e] = fma(cdt, k, base);
       }
-      for (int e = tid; e < I1_X * I1_Y; e += 32 * NCW) {   // v1 on (36 x 8)
-        const int x = e % I1_X, y = e / I1_X;                 // tile coords x-2, y
-        const int cr = (y + 4) * BR_X + x + 2;                // rho box origin (-4,-4)
-        const double k = d1s_(zR[2], cr, 1) * K.ih[0];
-        const double base = B ? sy[PY_R / 8 + e] : s1[(y + 2) * B1_X + x + 2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!r1_ok[u]) continue;
+        const int e = tid + u * NTC;
+        const double k = d1s_(zR[2], r1_cr[u], 1) * K.ih[0];
+        const double base = B ? sy[PYR + e] : s1[r1_b[u]];
         I1[e] = fma(cdt, k, base);
       }
-      for (int e = tid; e < I2_X * I2_Y; e += 32 * NCW) {   // v2 on (32 x 12)
-        const int x = e % I2_X, y = e / I2_X;                 // tile coords x, y-2
-        const int cr = (y + 2) * BR_X + x + 4;
-        const double k = d1s_(zR[2], cr, BR_X) * K.ih[1];
-        const double base = B ? sy[(PY_R + PY_1) / 8 + e] : s2[(y + 2) * B2_X + x + 2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!r2_ok[u]) continue;
+        const int e = tid + u * NTC;
+        const double k = d1s_(zR[2], r2_cr[u], BR_X) * K.ih[1];
+        const double base = B ? sy[PYR + PY1 + e] : s2[r2_b[u]];
         I2[e] = fma(cdt, k, base);
       }
-      for (int e = tid; e < I3_X * I3_Y; e += 32 * NCW) {   // v3 on (32 x 8)
-        const int x = e % I3_X, y = e / I3_X;
-        const int cr = (y + 4) * BR_X + x + 4;
+      {
         double dzr = 0.0;
 #pragma unroll
-        for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[2 + q][cr] - zR[2 - q][cr], dzr);
+        for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[2 + q][r3_cr] - zR[2 - q][r3_cr], dzr);
         const double k = dzr * K.ih[2];
-        const double base = B ? sy[(PY_R + PY_1 + PY_2) / 8 + e] : z3[2][(y + 2) * B3_X + x + 2];
-        I3[e] = fma(cdt, k, base);
+        const double base = B ? sy[PYR + PY1 + PY2 + tid] : z3[2][r3_b];
+        I3[tid] = fma(cdt, k, base);
       }
       cbar();  // the intermediate plane p is complete
       // ---- second stage at plane k = p - 2
       const int k = p - 2;
       if (k >= kb) {
-        const int ki = jj - 2;  // intermediate index of plane k
         const double* iR[5];
         const double* i3[5];
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
-          const unsigned char* sl = smem + G::OFF_IZ + ((ki - 2 + q + RI_Z) % RI_Z) * IZ_B;
-          iR[q] = reinterpret_cast<const double*>(sl);
-          i3[q] = reinterpret_cast<const double*>(sl + r128(IR_X * IR_Y * 8));
+          iR[q] = sm + OFF_IZD + izs[q] * IZD;
+          i3[q] = iR[q] + IR_D;
         }
-        const unsigned char* ipk = smem + G::OFF_IP + (ki % RI_P) * IP_B;
-        const double* i1 = reinterpret_cast<const double*>(ipk);
-        const double* i2 = reinterpret_cast<const double*>(ipk + r128(I1_X * I1_Y * 8));
-        const int cr = (tj + 2) * IR_X + ti + 2, c1 = tj * I1_X + ti + 2, c2 = (tj + 2) * I2_X + ti,
-                  c3 = tj * I3_X + ti;
+        const double* i1 = sm + OFF_IPD + ips[0] * IPD;
+        const double* i2 = i1 + I1_D;
         double S[5], kk[5];
-        S[GRHO] = iR[2][cr];
-        S[GV1] = i1[c1];
-        S[GV2] = i2[c2];
-        S[GV3] = i3[2][c3];
+        S[GRHO] = iR[2][s_cr];
+        S[GV1] = i1[s_c1];
+        S[GV2] = i2[s_c2];
+        S[GV3] = i3[2][s_c3];
         double dzr = 0.0, dv3 = 0.0;
 #pragma unroll
         for (int q = W; q >= 1; --q) {
-          dzr = fma(D1W<W>::c(q), iR[2 + q][cr] - iR[2 - q][cr], dzr);
-          dv3 = fma(D1W<W>::c(q), i3[2 + q][c3] - i3[2 - q][c3], dv3);
+          dzr = fma(D1W<W>::c(q), iR[2 + q][s_cr] - iR[2 - q][s_cr], dzr);
+          dv3 = fma(D1W<W>::c(q), i3[2 + q][s_c3] - i3[2 - q][s_c3], dv3);
         }
-        const double dxr = d1s_(iR[2], cr, 1) * K.ih[0];
-        const double dyr = d1s_(iR[2], cr, IR_X) * K.ih[1];
+        const double dxr = d1s_(iR[2], s_cr, 1) * K.ih[0];
+        const double dyr = d1s_(iR[2], s_cr, IR_X) * K.ih[1];
         dzr = dzr * K.ih[2];
-        const double dv1 = d1s_(i1, c1, 1) * K.ih[0];
-        const double dv2 = d1s_(i2, c2, I2_X) * K.ih[1];
+        const double dv1 = d1s_(i1, s_c1, 1) * K.ih[0];
+        const double dv2 = d1s_(i2, s_c2, I2_X) * K.ih[1];
         dv3 = dv3 * K.ih[2];
         kk[GRHO] = dv1 + dv2 + dv3;
         kk[GV1] = dxr;
@@ -297,27 +352,24 @@ __global__ void __launch_bounds__(NT, 1)
         kk[GV3] = dzr;
         double Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
         if (!B) {
-          // y at plane k: input ring planes k = p - 2 -> zR[0], P plane k = P ring index pi - 2
-          const unsigned char* pk = smem + G::OFF_P + ((pi - 2) % G::RP) * G::PSLOT;
-          const double* k1 = reinterpret_cast<const double*>(pk);
-          const double* k2 = reinterpret_cast<const double*>(pk + P1_B);
-          Y[GRHO] = zR[0][(tj + 4) * BR_X + ti + 4];
-          Y[GV1] = k1[(tj + 2) * B1_X + ti + 4];
-          Y[GV2] = k2[(tj + 4) * B2_X + ti + 2];
-          Y[GV3] = z3[0][(tj + 2) * B3_X + ti + 2];
+          // y at plane k: input plane k = p - 2 (zR[0]), P plane k (slot psl2)
+          const double* k1 = sm + OFF_PD + psl2 * PSD;
+          const double* k2 = k1 + P1D;
+          Y[GRHO] = zR[0][y_r];
+          Y[GV1] = k1[y_1];
+          Y[GV2] = k2[y_2];
+          Y[GV3] = z3[0][y_3];
         } else {
-          const uint32_t qi = nq;
-          mbar_wait(qfull + qi % G::RQ, (qi / G::RQ) & 1);
-          const double* qs = reinterpret_cast<const double*>(smem + G::OFF_Q + (qi % G::RQ) * G::QSLOT);
-          const int cc = tj * TX + ti;
+          mbar_wait(qfull + nq % G::RQ, (nq / G::RQ) & 1);
+          const double* qs = sm + OFF_QD + (nq % G::RQ) * (G::QSLOT / 8);
           // u carry of stage 3 (folded): Q.u += dt/3 C.rho, with C.rho at plane k from the ring
-          qu = fma(K.dt3, zR[0][(tj + 4) * BR_X + ti + 4], qs[cc]);
+          qu = fma(K.dt3, zR[0][y_r], qs[cc]);
 #pragma unroll
           for (int f = 1; f <= 4; ++f) Qv[f] = qs[f * C1 + cc];
           yu = qs[5 * C1 + cc];
         }
         if (live) {
-          const int64_t c = L.idx(i, j, k);
+          const int64_t c = cglob;
           const bool nf = near_face(L, i, j, k);
           if (!B) {
             double* outc = a.s.c;
@@ -341,19 +393,29 @@ __global__ void __launch_bounds__(NT, 1)
             wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
           }
         }
+        cglob += L.plane;
         __syncwarp();
         if (lane == 0) {
           if (B) mbar_arrive(qempty + nq % G::RQ);
-          mbar_arrive(pempty + (pi - 2) % G::RP);  // P plane k
+          mbar_arrive(pempty + psl2);  // P plane k
         }
         if (B) ++nq;
       } else if (jj < 2) {
         // planes kb-2, kb-1 never reach the second stage: free their P slots now
         __syncwarp();
-        if (lane == 0) mbar_arrive(pempty + pi % G::RP);
+        if (lane == 0) mbar_arrive(pempty + psl);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(zempty + (z0 + jj) % RZ);  // input plane p - 2
+      if (lane == 0) mbar_arrive(zempty + zsl[0]);  // input plane p - 2
+      // advance the rings: input planes shift by one, P slot of plane p+1, of plane p-1
+#pragma unroll
+      for (int q = 0; q < 4; ++q) zsl[q] = zsl[q + 1];
+      zsl[4] = zsl[3] + 1 == RZ ? 0 : zsl[3] + 1;
+      if (zsl[4] == 0) zph ^= 1;
+      // P slot of plane (p+1)-2 for the next iteration: ring index p0 + jj - 1
+      psl2 = (jj == 1) ? (int)(p0 % G::RP) : (psl2 + 1 == G::RP ? 0 : psl2 + 1);
+      psl = psl + 1 == G::RP ? 0 : psl + 1;
+      if (psl == 0) pph ^= 1;
     }
     // the last two P planes (ke, ke+1) and input planes ke .. ke+3 were only read
     __syncwarp();
