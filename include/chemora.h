@@ -193,10 +193,11 @@ int chemora_read_monitor(chemora_grid_t grid, double* out, int32_t max, int32_t*
                          void* stream);
 
 /* Model-driven tiling choice ("autotuning is model driven"): a
- * footprint/occupancy model prunes the stage-kernel tilings to <= 3 candidates, each is
+ * footprint/occupancy model prunes the stage-kernel tilings to <= 4 candidates, each is
  * timed on `trials` stage-1 launches (dt = 0: the state is not modified, the scratch set B
  * is), and the fastest is kept for this handle.  chosen[3] = {variant, band, #candidates};
- * ms_out (optional, >= 3 doubles) receives the best time per candidate.  Synchronises.
+ * ms_out (optional, >= 4 doubles) receives the best time per candidate (wave: per-step
+ * estimate from stage 1-3 timings, or the two pair kernels; BSSN: stage 1).  Synchronises.
  * With nranks > 1 every rank must call it at the same point of its call sequence. */
 int chemora_autotune(chemora_grid_t grid, int32_t trials, int32_t* chosen, double* ms_out,
                      void* stream);

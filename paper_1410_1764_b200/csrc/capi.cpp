@@ -398,7 +398,9 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->hi_flag = g->flags;
   g->ipc = false;
   g->cur = 0;
-  g->variant = 0;
+  // default tiling: the temporally blocked stage pairs for 4th-order wave grids (fastest
+  // measured, profiles/r1_wave_design_study.md), else one thread per point; BSSN: fission
+  g->variant = (desc->system == CHEMORA_SYS_WAVE && (desc->fd_order == 0 || desc->fd_order == 4)) ? kVariantFused : 0;
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
@@ -620,29 +622,56 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     if (order <= 4 && tiles >= 148) cands.push_back({4, 0});
+    if (order == 4 && g->L.g >= 4 && !g->monitor) cands.push_back({kVariantFused, 0});
   } else {
     cands.push_back({0, 0});
     if (g->L.nx * g->L.ny * g->L.nz <= (int64_t)64 * 64 * 64) cands.push_back({1, 0});
   }
   const int saved_v = g->variant, saved_b = g->band;
-  cudaEvent_t e0, e1;
+  cudaEvent_t e0, e1, e2;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventCreate(&e2));
   double best = 1e300;
   int besti = 0;
   for (size_t c = 0; c < cands.size(); ++c) {
     g->variant = cands[c].variant;
     g->band = cands[c].band;
-    StageLaunch a = stage_args(g, 0.0);  // dt = 0: stage 1 writes B = y, the state is untouched
-    CUDA_TRY(launch_stage(g, a, 1, st));
+    // dt = 0 and only launches that write scratch sets (B, C, Q): the state is untouched.
+    // Stage-wise candidates time stages 1-3 and model stage 4 as stage 3 scaled by its
+    // bytes (120 vs 112 B/pt); the temporally blocked candidate times both pair kernels
+    // (its new state lands in B and is not rotated in).
+    StageLaunch a = stage_args(g, 0.0);
+    const bool fusedc = cands[c].variant == kVariantFused;
+    auto run = [&](float* ms3) -> cudaError_t {
+      cudaError_t e = cudaSuccess;
+      if (fusedc) {
+        e = wave_fused_pair(a, 0, st);
+        if (e == cudaSuccess) e = wave_fused_pair(a, 1, st);
+        return e;
+      }
+      const int last = g->desc.system == CHEMORA_SYS_WAVE ? 3 : 1;
+      for (int s = 1; s <= last && e == cudaSuccess; ++s) {
+        if (s == 3 && ms3) e = cudaEventRecord(e2, st);
+        if (e == cudaSuccess) e = launch_stage(g, a, s, st);
+      }
+      return e;
+    };
+    CUDA_TRY(run(nullptr));
     float msmin = 1e30f;
     for (int t = 0; t < trials; ++t) {
+      float dummy = 0.f;
       CUDA_TRY(cudaEventRecord(e0, st));
-      CUDA_TRY(launch_stage(g, a, 1, st));
+      CUDA_TRY(run(&dummy));
       CUDA_TRY(cudaEventRecord(e1, st));
       CUDA_TRY(cudaEventSynchronize(e1));
       float ms = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      if (!fusedc && g->desc.system == CHEMORA_SYS_WAVE) {
+        float ms3 = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms3, e2, e1));
+        ms += ms3 * 120.f / 112.f;
+      }
       if (ms < msmin) msmin = ms;
     }
     if (ms_out) ms_out[c] = msmin;
@@ -650,6 +679,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
   (void)saved_v; (void)saved_b;
   g->variant = cands[besti].variant;
   g->band = cands[besti].band;
