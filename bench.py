@@ -43,6 +43,35 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def _traffic_table():
+    p = os.path.join(HERE, "profiles", "r1_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
+def measured_traffic(config: str, variant: int):
+    """DRAM bytes per step from the committed ncu capture of this config/variant (or None)."""
+    t = _traffic_table().get(config, {}).get(str(variant))
+    return None if t is None else t.get("dram_bytes_per_step")
+
+
+def bssn_fp64_roofline(pts: int, step_s: float):
+    """fp64-pipe roofline for the BSSN step: thread-level fp64 instructions per point-update
+    (ncu sm__inst_executed_pipe_fp64 x 32 / points, committed in profiles/r1_traffic.json)
+    vs 148 SMs x 64 fp64 lanes x the max SM clock."""
+    t = _traffic_table().get("bssn192", {}).get("fp64_thread_instr_per_point_step")
+    if not t:
+        return {}
+    peak_inst = 148 * 64 * 1.965e9  # fp64 thread-instructions / s at max clock (DFMA = 2 flops)
+    achieved = t * pts / step_s
+    return {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_inst / 1e12,
+            "unit": "T fp64 thread-instr/s", "frac": achieved / peak_inst,
+            "fp64_instr_per_point_step": t,
+            "hbm_frac_at_2400_bytes": 2400 * pts / step_s / 1e9 / measured_peaks()[0]}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -236,16 +265,31 @@ def main():
     pts_local = n[0] * n[1] * n[2]
     value = pts_local * world * args.steps / (total_ms * 1e-3)
 
-    # roofline of the dominant kernel: the 4 fused stage kernels of one RK4 step
+    # roofline of the dominant kernel(s): the kernels of one RK4 step are the only launches in
+    # the timed region.  Algorithmic bytes are those of the active kernel design: 432 B/pt for
+    # one kernel per RK stage, 256 B/pt for the temporally blocked stage
+    # pairs -- the frac is against that design's own HBM floor.
     peak, peak_kind = measured_peaks()
     mean_step_s = float(np.mean(step_ms)) * 1e-3
-    bpp = BYTES_PER_POINT[cfg["system"]]
+    variant = g.kernel_variant()
+    floor_bpp = BYTES_PER_POINT[cfg["system"]]
+    bpp = 256 if (cfg["system"] == "wave" and variant == 6) else floor_bpp
     achieved = bpp * pts_local / mean_step_s / 1e9
+    traffic = measured_traffic(args.config, variant)
+    kname = ("wave_fused<A>, wave_fused<B> (2 launches = 1 step)" if bpp == 256 else
+             "stage kernels (4 launches x groups = 1 step)")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                "kernel": "fused RK4 stage kernels (4 launches = 1 step)",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                "kernel": kname, "variant": variant,
                 "algorithmic_bytes_per_point": bpp,
+                "traffic_note": "ncu dram__bytes_read+write per step (all launches of one step), profiles/r1_traffic.json",
+                "one_pass_per_stage_bytes_per_point": floor_bpp,
+                "frac_at_one_pass_per_stage_bytes": floor_bpp * pts_local / mean_step_s / 1e9 / peak,
                 "frac_of_nominal_8TBps": achieved / 8000.0}
+    if cfg["system"] == "bssn":
+        # BSSN is bound by the fp64 pipe: fp64 instructions per point-update
+        # counted by ncu (profiles/r1_traffic.json) against 64 DFMA lanes/SM/clock.
+        roofline.update(bssn_fp64_roofline(pts_local, mean_step_s))
 
     # e2e through the public API with host buffers: per step, upload the state from pinned
     # host memory, one RK4 step, download the state.

@@ -73,6 +73,7 @@ _SIGS = {
     "chemora_set_kernel_variant": ([_vp, ctypes.c_int], ctypes.c_int),
     "chemora_set_monitor": ([_vp, ctypes.c_int], ctypes.c_int),
     "chemora_debug_get_set": ([_vp, ctypes.c_int, _dp, _vp], ctypes.c_int),
+    "chemora_get_kernel_variant": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "chemora_read_monitor": ([_vp, _dp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
     "chemora_autotune": ([_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _dp, _vp], ctypes.c_int),
 }

@@ -436,6 +436,13 @@ int chemora_grid_local(chemora_grid_t g, int64_t* ext, int64_t* z0) {
   return CHEMORA_OK;
 }
 
+int chemora_get_kernel_variant(chemora_grid_t g, int* variant) {
+  if (int rc = check_grid(g)) return rc;
+  if (!variant) return fail(CHEMORA_E_INVALID, "variant is NULL");
+  *variant = use_fused(g) ? kVariantFused : (g->variant == kVariantFused ? 0 : g->variant);
+  return CHEMORA_OK;
+}
+
 int chemora_set_kernel_variant(chemora_grid_t g, int variant) {
   if (int rc = check_grid(g)) return rc;
   g->variant = variant;

@@ -85,6 +85,11 @@ class Grid:
     def set_kernel_variant(self, v):
         C.chemora_set_kernel_variant(self.handle, v)
 
+    def kernel_variant(self) -> int:
+        v = C.ctypes.c_int()
+        C._check(C._lib.chemora_get_kernel_variant(self.handle, C.ctypes.byref(v)), "chemora_get_kernel_variant")
+        return v.value
+
     def set_monitor(self, enable=True):
         C.chemora_set_monitor(self.handle, enable)
 
