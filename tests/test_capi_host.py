@@ -53,16 +53,20 @@ def _desc(**kw):
 
 
 def test_required_bytes_layout():
-    """4 sets x 5 GFs of padded arrays: Px = round_up(16 + N + g, 16), Py = Pz = N + 2g."""
+    """4 sets x 5 GFs of padded arrays: Px = round_up(16 + N + gs, 16), Py = Pz = N + 2gs with
+    the storage ghost gs = max(g, 4) of 4th-order wave grids."""
     _ensure_built()
     from paper_1410_1764_b200 import capi as C
     n = C.chemora_grid_required_bytes(_desc())
-    px, py, pz = 64, 38, 38
+    px, py, pz = 64, 40, 40
     arr = ((px * py * pz + 31) // 32) * 32 * 8
     assert n >= 4 * 5 * arr
-    assert n < 4 * 5 * arr + 200_000
+    assert n < 4 * 5 * arr + 300_000
     n512 = C.chemora_grid_required_bytes(_desc(extent=(512, 512, 512)))
-    assert 23.0e9 < n512 < 23.6e9  # fits one B200 with room to spare
+    assert 23.0e9 < n512 < 23.8e9  # fits one B200 with room to spare
+    # 2nd-order grids keep g = 3 (radius 1)
+    n2 = C.chemora_grid_required_bytes(_desc(fd_order=2))
+    assert n2 < n
 
 
 @pytest.mark.parametrize("kw,code", [
