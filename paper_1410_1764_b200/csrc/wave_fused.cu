@@ -13,7 +13,7 @@
 // This is the kernel fusion of PAPER.md:537-547 carried across RK stages.
 //
 // Structure (both kernels): persistent, one CTA per SM walks (tile 32x8, z chunk) items; a
-// producer thread streams the inputs with TMA into mbarrier rings; sixteen consumer warps
+// producer thread streams the inputs with TMA into mbarrier rings; eight consumer warps
 // first compute the intermediate state on the tile extended by the stencil radius for plane
 // p = k + 2 (z-derivatives of the inputs from the ring's neighbouring planes), then the
 // second stage at plane k from the intermediate-state ring.  The per-point operation
@@ -32,7 +32,7 @@ namespace chemora {
 namespace {
 using namespace wave;
 
-constexpr int TX = 32, TY = 8, NCW = 16, NT = 32 * (NCW + 1);
+constexpr int TX = 32, TY = 8, NCW = 8, NT = 32 * (NCW + 1);
 constexpr int W = 2;   // 4th-order stencils (fd_order 4 only)
 constexpr int H = 4;   // input halo: two stacked radius-2 stencils
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
@@ -108,10 +108,9 @@ __global__ void __launch_bounds__(NT, 1)
   const Layout& L = a.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    // empty barriers: one arrival per release (thread 0, after a consumer-wide bar.sync)
-    for (int s = 0; s < RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, 1); }
-    for (int s = 0; s < G::RP; ++s) { mbar_init(pfull + s, 1); mbar_init(pempty + s, 1); }
-    for (int s = 0; s < G::RQ; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, 1); }
+    for (int s = 0; s < RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, NCW); }
+    for (int s = 0; s < G::RP; ++s) { mbar_init(pfull + s, 1); mbar_init(pempty + s, NCW); }
+    for (int s = 0; s < G::RQ; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, NCW); }
     fence_mbar_init();
   }
   __syncthreads();
@@ -175,36 +174,50 @@ __global__ void __launch_bounds__(NT, 1)
   }
 
   // --------------------------------------------------------------------------- consumers
-  // 16 consumer warps.  Intermediate state: one element per thread per region (offsets are
-  // per-thread constants).  Second stage: two threads per tile point -- half 0 computes the
-  // rho and v1 equations (and the u carry), half 1 the v2 and v3 equations -- so each thread
-  // carries half the stencils.  Ring slots advance by increment-and-wrap.
+  // All shared-memory offsets below are per-thread constants (computed once); the ring
+  // slots advance by increment-and-wrap, so the per-plane loop is loads, flops and stores.
   const int tid = threadIdx.x;
   const int64_t gfs = L.gfs;
   constexpr int NTC = 32 * NCW;
   constexpr int IRN = IR_X * IR_Y, I1N = I1_X * I1_Y, I2N = I2_X * I2_Y, I3N = I3_X * I3_Y;
-  static_assert(IRN <= NTC && I1N <= NTC && I2N <= NTC && I3N <= NTC, "tile geometry");
-  const bool rR_ok = tid < IRN, r1_ok = tid < I1N, r2_ok = tid < I2N, r3_ok = tid < I3N;
-  int rR_c1, rR_c2, rR_c3, rR_b, r1_cr, r1_b, r2_cr, r2_b, r3_cr, r3_b;
-  {
-    int x = tid % IR_X, y = tid / IR_X;
-    rR_c1 = y * B1_X + x + 2;
-    rR_c2 = (y + 2) * B2_X + x;
-    rR_c3 = y * B3_X + x;
-    rR_b = (y + 2) * BR_X + x + 2;
-    x = tid % I1_X; y = tid / I1_X;
-    r1_cr = (y + 4) * BR_X + x + 2;
-    r1_b = (y + 2) * B1_X + x + 2;
-    x = tid % I2_X; y = tid / I2_X;
-    r2_cr = (y + 2) * BR_X + x + 4;
-    r2_b = (y + 2) * B2_X + x + 2;
-    x = tid % I3_X; y = tid / I3_X;
-    r3_cr = (y + 4) * BR_X + x + 4;
-    r3_b = (y + 2) * B3_X + x + 2;
+  static_assert(IRN <= 2 * NTC && I1N <= 2 * NTC && I2N <= 2 * NTC && I3N == NTC, "tile geometry");
+  // intermediate rho elements e = tid, tid + NTC: offsets into v1/v2/v3/rho(or y) boxes
+  int rR_c1[2], rR_c2[2], rR_c3[2], rR_b[2];
+  bool rR_ok[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * NTC;
+    rR_ok[u] = e < IRN;
+    const int x = e % IR_X, y = e / IR_X;
+    rR_c1[u] = y * B1_X + x + 2;
+    rR_c2[u] = (y + 2) * B2_X + x;
+    rR_c3[u] = y * B3_X + x;
+    rR_b[u] = (y + 2) * BR_X + x + 2;
   }
-  // second stage: point (ti, tj) of the tile, equation half
-  const int half = warp >> 3;
-  const int ti = lane, tj = warp & 7;
+  int r1_cr[2], r1_b[2];
+  bool r1_ok[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * NTC;
+    r1_ok[u] = e < I1N;
+    const int x = e % I1_X, y = e / I1_X;
+    r1_cr[u] = (y + 4) * BR_X + x + 2;
+    r1_b[u] = (y + 2) * B1_X + x + 2;
+  }
+  int r2_cr[2], r2_b[2];
+  bool r2_ok[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * NTC;
+    r2_ok[u] = e < I2N;
+    const int x = e % I2_X, y = e / I2_X;
+    r2_cr[u] = (y + 2) * BR_X + x + 4;
+    r2_b[u] = (y + 2) * B2_X + x + 2;
+  }
+  const int r3_cr = (tid / I3_X + 4) * BR_X + tid % I3_X + 4;
+  const int r3_b = (tid / I3_X + 2) * B3_X + tid % I3_X + 2;
+  // second stage: this thread's point (ti, tj) of the tile
+  const int ti = lane, tj = warp;
   const int s_cr = (tj + 2) * IR_X + ti + 2, s_c1 = tj * I1_X + ti + 2, s_c2 = (tj + 2) * I2_X + ti,
             s_c3 = tj * I3_X + ti;
   const int y_r = (tj + 4) * BR_X + ti + 4, y_1 = (tj + 2) * B1_X + ti + 4, y_2 = (tj + 4) * B2_X + ti + 2,
@@ -228,6 +241,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
     int64_t cglob = L.idx(i, j, kb);  // global offset of this thread's point at plane k
+    // ring slots: input planes p-2..p+2, P planes p and p-2, intermediate planes
     int zsl[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) zsl[q] = (int)((z0 + q) % RZ);
@@ -236,16 +250,16 @@ __global__ void __launch_bounds__(NT, 1)
     int pph = (int)((p0 / G::RP) & 1);
     int izs[5] = {0, 0, 0, 0, 0};           // intermediate z slots of planes p-4..p
     int ips[3] = {0, 0, 0};                 // intermediate p slots of planes p-2..p
-    int izn = 0, ipn = 0;                   // slot of plane p (jj mod 5, jj mod 3)
 #pragma unroll 1
     for (int jj = 0; jj < nk + 4; ++jj) {
       const int p = kb - 2 + jj;
+      // intermediate slot of plane p (jj mod 5 / mod 3), kept incrementally
 #pragma unroll
       for (int q = 0; q < 4; ++q) izs[q] = izs[q + 1];
-      izs[4] = izn;
+      izs[4] = jj % RI_Z;
       ips[0] = ips[1];
       ips[1] = ips[2];
-      ips[2] = ipn;
+      ips[2] = jj % RI_P;
       mbar_wait(zfull + zsl[4], zph);
       mbar_wait(pfull + psl, pph);
       const double* zR[5];
@@ -258,34 +272,43 @@ __global__ void __launch_bounds__(NT, 1)
       const double* s1 = sm + OFF_PD + psl * PSD;
       const double* s2 = s1 + P1D;
       const double* sy = s2 + P2D;  // B only
-      double* IR = sm + OFF_IZD + izn * IZD;
+      double* IR = sm + OFF_IZD + izs[4] * IZD;
       double* I3 = IR + IR_D;
-      double* I1 = sm + OFF_IPD + ipn * IPD;
+      double* I1 = sm + OFF_IPD + ips[2] * IPD;
       double* I2 = I1 + I1_D;
       cbar();  // everyone is done with the intermediate slots being overwritten
       // ---- intermediate state at plane p: Y2 = y + dt/2 k1(y) (A) or Y4 = y + dt k3(C) (B)
-      if (rR_ok) {
-        const double dv1 = d1s_(s1, rR_c1, 1) * K.ih[0];
-        const double dv2 = d1s_(s2, rR_c2, B2_X) * K.ih[1];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!rR_ok[u]) continue;
+        const double dv1 = d1s_(s1, rR_c1[u], 1) * K.ih[0];
+        const double dv2 = d1s_(s2, rR_c2[u], B2_X) * K.ih[1];
         double dv3 = 0.0;
 #pragma unroll
-        for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][rR_c3] - z3[2 - q][rR_c3], dv3);
+        for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][rR_c3[u]] - z3[2 - q][rR_c3[u]], dv3);
         dv3 = dv3 * K.ih[2];
         const double k = dv1 + dv2 + dv3;
-        const double base = B ? sy[tid] : zR[2][rR_b];
-        IR[tid] = fma(cdt, k, base);
+        const int e = tid + u * NTC;
+        const double base = B ? sy[e] : zR[2][rR_b[u]];
+        IR[e] = fma(cdt, k, base);
       }
-      if (r1_ok) {
-        const double k = d1s_(zR[2], r1_cr, 1) * K.ih[0];
-        const double base = B ? sy[PYR + tid] : s1[r1_b];
-        I1[tid] = fma(cdt, k, base);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!r1_ok[u]) continue;
+        const int e = tid + u * NTC;
+        const double k = d1s_(zR[2], r1_cr[u], 1) * K.ih[0];
+        const double base = B ? sy[PYR + e] : s1[r1_b[u]];
+        I1[e] = fma(cdt, k, base);
       }
-      if (r2_ok) {
-        const double k = d1s_(zR[2], r2_cr, BR_X) * K.ih[1];
-        const double base = B ? sy[PYR + PY1 + tid] : s2[r2_b];
-        I2[tid] = fma(cdt, k, base);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!r2_ok[u]) continue;
+        const int e = tid + u * NTC;
+        const double k = d1s_(zR[2], r2_cr[u], BR_X) * K.ih[1];
+        const double base = B ? sy[PYR + PY1 + e] : s2[r2_b[u]];
+        I2[e] = fma(cdt, k, base);
       }
-      if (r3_ok) {
+      {
         double dzr = 0.0;
 #pragma unroll
         for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[2 + q][r3_cr] - zR[2 - q][r3_cr], dzr);
@@ -294,116 +317,109 @@ __global__ void __launch_bounds__(NT, 1)
         I3[tid] = fma(cdt, k, base);
       }
       cbar();  // the intermediate plane p is complete
-      // ---- second stage at plane k = p - 2 (same operation sequence as wave_update)
+      // ---- second stage at plane k = p - 2
       const int k = p - 2;
       if (k >= kb) {
-        const double* iR2 = sm + OFF_IZD + izs[2] * IZD;  // intermediate plane k
+        const double* iR[5];
+        const double* i3[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          iR[q] = sm + OFF_IZD + izs[q] * IZD;
+          i3[q] = iR[q] + IR_D;
+        }
         const double* i1 = sm + OFF_IPD + ips[0] * IPD;
         const double* i2 = i1 + I1_D;
-        double* out;
-        FaceDst fd;
-        if (!B) { out = a.s.c; fd = a.img[1]; }
-        else { out = a.s.b; fd = a.img[0]; }  // new state -> scratch set (rotated by the caller)
-        const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
-        const bool nf = live && near_face(L, i, j, k);
-        const int64_t c = cglob;
-        auto put = [&](int f, double v) {
-          out[f * gfs + c] = v;
-          if (nf) store_images(out + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
-          if (B) check_finite(a.nan_flag, code0 + f, v);
-        };
-        double qv[5], yv = 0.0, qu = 0.0;
-        if (B) {
+        double S[5], kk[5];
+        S[GRHO] = iR[2][s_cr];
+        S[GV1] = i1[s_c1];
+        S[GV2] = i2[s_c2];
+        S[GV3] = i3[2][s_c3];
+        double dzr = 0.0, dv3 = 0.0;
+#pragma unroll
+        for (int q = W; q >= 1; --q) {
+          dzr = fma(D1W<W>::c(q), iR[2 + q][s_cr] - iR[2 - q][s_cr], dzr);
+          dv3 = fma(D1W<W>::c(q), i3[2 + q][s_c3] - i3[2 - q][s_c3], dv3);
+        }
+        const double dxr = d1s_(iR[2], s_cr, 1) * K.ih[0];
+        const double dyr = d1s_(iR[2], s_cr, IR_X) * K.ih[1];
+        dzr = dzr * K.ih[2];
+        const double dv1 = d1s_(i1, s_c1, 1) * K.ih[0];
+        const double dv2 = d1s_(i2, s_c2, I2_X) * K.ih[1];
+        dv3 = dv3 * K.ih[2];
+        kk[GRHO] = dv1 + dv2 + dv3;
+        kk[GV1] = dxr;
+        kk[GV2] = dyr;
+        kk[GV3] = dzr;
+        double Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
+        if (!B) {
+          // y at plane k: input plane k = p - 2 (zR[0]), P plane k (slot psl2)
+          const double* k1 = sm + OFF_PD + psl2 * PSD;
+          const double* k2 = k1 + P1D;
+          Y[GRHO] = zR[0][y_r];
+          Y[GV1] = k1[y_1];
+          Y[GV2] = k2[y_2];
+          Y[GV3] = z3[0][y_3];
+        } else {
           mbar_wait(qfull + nq % G::RQ, (nq / G::RQ) & 1);
           const double* qs = sm + OFF_QD + (nq % G::RQ) * (G::QSLOT / 8);
+          // u carry of stage 3 (folded): Q.u += dt/3 C.rho, with C.rho at plane k from the ring
+          qu = fma(K.dt3, zR[0][y_r], qs[cc]);
 #pragma unroll
-          for (int f = 1; f <= 4; ++f) qv[f] = qs[f * C1 + cc];
-          if (half == 0) {
-            // u carry of stage 3 (folded): Q.u += dt/3 C.rho (C.rho at plane k from the ring)
-            qu = fma(K.dt3, zR[0][y_r], qs[cc]);
-            yv = qs[5 * C1 + cc];
-          }
+          for (int f = 1; f <= 4; ++f) Qv[f] = qs[f * C1 + cc];
+          yu = qs[5 * C1 + cc];
         }
-        if (half == 0) {
-          // rho (k = d1 v1 + d1 v2 + d1 v3) and v1 (k = d1x rho); u carry
-          const double* i3[5];
-#pragma unroll
-          for (int q = 0; q < 5; ++q) i3[q] = sm + OFF_IZD + izs[q] * IZD + IR_D;
-          double dv3 = 0.0;
-#pragma unroll
-          for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), i3[2 + q][s_c3] - i3[2 - q][s_c3], dv3);
-          const double dv1 = d1s_(i1, s_c1, 1) * K.ih[0];
-          const double dv2 = d1s_(i2, s_c2, I2_X) * K.ih[1];
-          dv3 = dv3 * K.ih[2];
-          const double krho = dv1 + dv2 + dv3;
-          const double kv1 = d1s_(iR2, s_cr, 1) * K.ih[0];
-          const double Srho = iR2[s_cr], Sv1 = i1[s_c1];
-          if (live) {
-            if (!B) {
-              const double* k1 = sm + OFF_PD + psl2 * PSD;
-              const double Yrho = zR[0][y_r], Yv1 = k1[y_1];
-              a.s.q[GRHO * gfs + c] = fma(K.dt3, krho, (Yrho + Srho) * K.third);
-              put(GRHO, fma(K.dt2, krho, Yrho));
-              a.s.q[GV1 * gfs + c] = fma(K.dt3, kv1, (Yv1 + Sv1) * K.third);
-              put(GV1, fma(K.dt2, kv1, Yv1));
-              a.s.q[c] = fma(K.dt3, Srho, K.dt6 * Yrho);
-            } else {
-              put(GRHO, fma(K.dt6, krho, fma(Srho, K.third, qv[GRHO])));
-              put(GV1, fma(K.dt6, kv1, fma(Sv1, K.third, qv[GV1])));
-              put(GU, fma(K.dt6, Srho, yv + qu));
-            }
-          }
-        } else {
-          // v2 (k = d1y rho) and v3 (k = d1z rho)
-          const double* iR[5];
-#pragma unroll
-          for (int q = 0; q < 5; ++q) iR[q] = sm + OFF_IZD + izs[q] * IZD;
-          double dzr = 0.0;
-#pragma unroll
-          for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), iR[2 + q][s_cr] - iR[2 - q][s_cr], dzr);
-          const double kv2 = d1s_(iR2, s_cr, IR_X) * K.ih[1];
-          const double kv3 = dzr * K.ih[2];
-          const double Sv2 = i2[s_c2], Sv3 = iR2[IR_D + s_c3];
-          if (live) {
-            if (!B) {
-              const double* k1 = sm + OFF_PD + psl2 * PSD;
-              const double Yv2 = k1[P1D + y_2], Yv3 = z3[0][y_3];
-              a.s.q[GV2 * gfs + c] = fma(K.dt3, kv2, (Yv2 + Sv2) * K.third);
-              put(GV2, fma(K.dt2, kv2, Yv2));
-              a.s.q[GV3 * gfs + c] = fma(K.dt3, kv3, (Yv3 + Sv3) * K.third);
-              put(GV3, fma(K.dt2, kv3, Yv3));
-            } else {
-              put(GV2, fma(K.dt6, kv2, fma(Sv2, K.third, qv[GV2])));
-              put(GV3, fma(K.dt6, kv3, fma(Sv3, K.third, qv[GV3])));
-            }
+        if (live) {
+          const int64_t c = cglob;
+          const bool nf = near_face(L, i, j, k);
+          if (!B) {
+            double* outc = a.s.c;
+            const FaceDst fd = a.img[1];
+            auto put = [&](int f, double v) {
+              outc[f * gfs + c] = v;
+              if (nf) store_images(outc + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+            };
+            auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
+            wave_update<2>(K, S, kk, Y, Qv, yu, qu, put, putq);
+          } else {
+            double* outy = a.s.b;  // the new state goes to the scratch set (swapped by the caller)
+            const FaceDst fd = a.img[0];
+            const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
+            auto put = [&](int f, double v) {
+              outy[f * gfs + c] = v;
+              if (nf) store_images(outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
+              check_finite(a.nan_flag, code0 + f, v);
+            };
+            auto putq = [&](int, double) {};
+            wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
           }
         }
         cglob += L.plane;
-        cbar();  // both halves are done with this plane's ring slots
-        if (tid == 0) {
+        __syncwarp();
+        if (lane == 0) {
           if (B) mbar_arrive(qempty + nq % G::RQ);
           mbar_arrive(pempty + psl2);  // P plane k
         }
         if (B) ++nq;
       } else if (jj < 2) {
         // planes kb-2, kb-1 never reach the second stage: free their P slots now
-        if (tid == 0) mbar_arrive(pempty + psl);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pempty + psl);
       }
-      if (tid == 0) mbar_arrive(zempty + zsl[0]);  // input plane p - 2 (all reads done: cbar)
-      // advance the rings
+      __syncwarp();
+      if (lane == 0) mbar_arrive(zempty + zsl[0]);  // input plane p - 2
+      // advance the rings: input planes shift by one, P slot of plane p+1, of plane p-1
 #pragma unroll
       for (int q = 0; q < 4; ++q) zsl[q] = zsl[q + 1];
       zsl[4] = zsl[3] + 1 == RZ ? 0 : zsl[3] + 1;
       if (zsl[4] == 0) zph ^= 1;
+      // P slot of plane (p+1)-2 for the next iteration: ring index p0 + jj - 1
       psl2 = (jj == 1) ? (int)(p0 % G::RP) : (psl2 + 1 == G::RP ? 0 : psl2 + 1);
       psl = psl + 1 == G::RP ? 0 : psl + 1;
       if (psl == 0) pph ^= 1;
-      izn = izn + 1 == RI_Z ? 0 : izn + 1;
-      ipn = ipn + 1 == RI_P ? 0 : ipn + 1;
     }
     // the last two P planes (ke, ke+1) and input planes ke .. ke+3 were only read
-    cbar();
-    if (tid == 0) {
+    __syncwarp();
+    if (lane == 0) {
       for (int q = 0; q < 2; ++q) mbar_arrive(pempty + (p0 + nk + 2 + q) % G::RP);
       for (int q = 0; q < 4; ++q) mbar_arrive(zempty + (z0 + nk + 4 + q) % RZ);
     }
