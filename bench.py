@@ -286,6 +286,12 @@ def main():
                 "one_pass_per_stage_bytes_per_point": floor_bpp,
                 "frac_at_one_pass_per_stage_bytes": floor_bpp * pts_local / mean_step_s / 1e9 / peak,
                 "frac_of_nominal_8TBps": achieved / 8000.0}
+    # our kernel launches per RK4 step: wave 2 (stage pairs) or 4 (one per stage); BSSN
+    # 3 fissioned groups x 4 stages, or 4 with the fused single kernel (variant 1)
+    if cfg["system"] == "wave":
+        launches_per_step = 2 if variant == 6 else 4
+    else:
+        launches_per_step = 4 if variant == 1 else 12
     if cfg["system"] == "bssn":
         # BSSN is bound by the fp64 pipe: fp64 instructions per point-update
         # counted by ncu (profiles/r1_traffic.json) against 64 DFMA lanes/SM/clock.
@@ -330,7 +336,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": cfgout, "roofline": roofline, "cpu_baseline": cb,
-                "e2e": e2e, "gpu_launches": 4 * args.steps, "clocks": clk.summary(),
+                "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
                 "step_ms": step_ms}
         print(json.dumps(line), flush=True)
     if world > 1:
