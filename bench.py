@@ -287,11 +287,12 @@ def main():
                 "frac_at_one_pass_per_stage_bytes": floor_bpp * pts_local / mean_step_s / 1e9 / peak,
                 "frac_of_nominal_8TBps": achieved / 8000.0}
     # our kernel launches per RK4 step: wave 2 (stage pairs) or 4 (one per stage); BSSN
-    # 3 fissioned groups x 4 stages, or 4 with the fused single kernel (variant 1)
+    # 4 (two-phase table kernel, variant 0, or fused single kernel, 1) or 3 fissioned
+    # groups x 4 stages (variant 2)
     if cfg["system"] == "wave":
         launches_per_step = 2 if variant == 6 else 4
     else:
-        launches_per_step = 4 if variant == 1 else 12
+        launches_per_step = 12 if variant == 2 else 4
     if cfg["system"] == "bssn":
         # BSSN is bound by the fp64 pipe: fp64 instructions per point-update
         # counted by ncu (profiles/r1_traffic.json) against 64 DFMA lanes/SM/clock.

@@ -9,9 +9,17 @@
 //   stage 3 (in C): B = y + dt k3
 //   stage 4 (in B): y = Q + B/3 + dt/6 k4
 //
-// The RHS is written on symmetric-packed tensors (xx, xy, xz, yy, yz, zz) with the
-// advection term evaluated branch-free as beta * S f + |beta| * A f, where
-// S = (D+ + D-)/2 and A = (D+ - D-)/2 (identical to max(beta,0) D+ + min(beta,0) D-).
+// The RHS algebra (bssn_point) is written once, on symmetric-packed tensors (xx, xy, xz,
+// yy, yz, zz), against a derivative *provider*:
+//   StencilP -- every derivative evaluated from global memory at the point (used by the
+//               one-thread-per-point kernels: fused G0 and fissioned G1/G2/G3);
+//   TabP     -- derivatives read from a shared-memory table that the CTA filled first
+//               (the two-phase kernel: phase 1 computes the 161 point values, first and
+//               second derivatives and advection terms of 32 points with fully parallel,
+//               register-light stencil evaluations; phase 2 runs the algebra, two threads
+//               per point splitting the equations).
+// Advection is evaluated branch-free as beta * S f + |beta| * A f with S = (D+ + D-)/2 and
+// A = (D+ - D-)/2 (identical to max(beta,0) D+ + min(beta,0) D-).
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -76,49 +84,91 @@ __device__ __forceinline__ double ADVraw(const double* __restrict__ f, int64_t c
   return fma(beta, S, fabs(beta) * A);
 }
 
-__device__ __forceinline__ double adv(const double* __restrict__ f, int64_t c, const Strides& st,
-                                      const double* beta, double f0, const BssnK& K) {
-  double r = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) r = fma(ADVraw(f, c, st.s[a], f0, beta[a]), K.i24h[a], r);
-  return r;
+// ------------------------------------------------------------------ derivative table
+// slots: [0,25) point values; [25,70) D1 of the 15 differentiated GFs x 3 axes; [70,136)
+// second derivatives of the 11 twice-differentiated GFs x 6 pairs; [136,161) Adv(gf).
+constexpr int T_D1 = 25, T_DD = 70, T_ADV = 136, NSLOT = 161;
+__host__ __device__ constexpr int d1i(int gf) {  // index in the D1 list
+  return gf == V_PHI ? 0 : (gf >= V_GT && gf < V_GT + 6) ? 1 + gf - V_GT : gf == V_TRK ? 7
+       : gf == V_ALPHA ? 8 : (gf >= V_BETA && gf < V_BETA + 3) ? 9 + gf - V_BETA
+       : (gf >= V_XT && gf < V_XT + 3) ? 12 + gf - V_XT : -1;
 }
+__host__ __device__ constexpr int d1gf(int i) {
+  return i == 0 ? V_PHI : i <= 6 ? V_GT + i - 1 : i == 7 ? V_TRK : i == 8 ? V_ALPHA : i <= 11 ? V_BETA + i - 9 : V_XT + i - 12;
+}
+__host__ __device__ constexpr int ddi(int gf) {  // index in the second-derivative list
+  return gf == V_PHI ? 0 : (gf >= V_GT && gf < V_GT + 6) ? 1 + gf - V_GT : gf == V_ALPHA ? 7
+       : (gf >= V_BETA && gf < V_BETA + 3) ? 8 + gf - V_BETA : -1;
+}
+__host__ __device__ constexpr int ddgf(int i) {
+  return i == 0 ? V_PHI : i <= 6 ? V_GT + i - 1 : i == 7 ? V_ALPHA : V_BETA + i - 8;
+}
+
+struct StencilP {
+  const double* in;
+  int64_t gfs, c;
+  Strides st;
+  const BssnK* K;
+  __device__ __forceinline__ double v(int gf) const { return ld(in + gf * gfs + c); }
+  __device__ __forceinline__ double d1(int gf, int l) const {
+    return D1raw(in + gf * gfs, c, st.s[l]) * K->i12h[l];
+  }
+  __device__ __forceinline__ double dd(int gf, int l, int m, double f0) const {
+    return (l == m) ? D2raw(in + gf * gfs, c, st.s[l], f0) * K->i12h2[l]
+                    : D11raw(in + gf * gfs, c, st.s[l], st.s[m]) * K->i144hh[l + m - 1];
+  }
+  __device__ __forceinline__ double adv(int gf, const double* beta, double f0) const {
+    double r = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) r = fma(ADVraw(in + gf * gfs, c, st.s[a], f0, beta[a]), K->i24h[a], r);
+    return r;
+  }
+};
+
+template <int NP>
+struct TabP {
+  const double* tab;  // [NSLOT][NP]
+  int pt;
+  __device__ __forceinline__ double v(int gf) const { return tab[gf * NP + pt]; }
+  __device__ __forceinline__ double d1(int gf, int l) const { return tab[(T_D1 + 3 * d1i(gf) + l) * NP + pt]; }
+  __device__ __forceinline__ double dd(int gf, int l, int m, double) const {
+    return tab[(T_DD + 6 * ddi(gf) + sy(l, m)) * NP + pt];
+  }
+  __device__ __forceinline__ double adv(int gf, const double*, double) const { return tab[(T_ADV + gf) * NP + pt]; }
+};
 
 // Output groups of the kernel fission (fission is "the most
 // important performance optimization" for the Einstein equations).
-// G0 = everything in one kernel; G1 = phi, gt, alpha, beta (kinematics, first
-// derivatives only); G2 = trK, At, A (curvature: Ricci, D_i D_j alpha); G3 = Xt, B
-// (second derivatives of the shift).
+// G0 = everything; G1 = phi, gt, alpha, beta (kinematics, first derivatives only);
+// G2 = trK, At, A (curvature: Ricci, D_i D_j alpha); G3 = Xt, B (second derivatives of
+// the shift); G13 = G1 + G3.
 __host__ __device__ constexpr bool in_group(int G, int v) {
   return G == 0 ? true
        : G == 1 ? (v == V_PHI || (v >= V_GT && v < V_GT + 6) || v == V_ALPHA || (v >= V_BETA && v < V_BETA + 3))
        : G == 2 ? (v == V_TRK || (v >= V_AT && v < V_AT + 6) || v == V_AUX)
-                : ((v >= V_XT && v < V_XT + 3) || (v >= V_B && v < V_B + 3));
+       : G == 3 ? ((v >= V_XT && v < V_XT + 3) || (v >= V_B && v < V_B + 3))
+                : (in_group(1, v) || in_group(3, v));
 }
 
-// Evaluate the right-hand sides of group G at interior offset c of the input set `in`
-// (advection included); rhs[v] is written for every v in the group.  App. A.2-A.3.
-template <int G>
-__device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_t gfs, int64_t c,
-                                           const Strides& st, const BssnK& K, double* rhs) {
-  constexpr bool g1 = G == 0 || G == 1, g2 = G == 0 || G == 2, g3 = G == 0 || G == 3;
-  auto F = [&](int v) { return in + v * gfs; };
+// Right-hand sides of group G from the derivative provider P (advection included);
+// rhs[v] is written for every v in the group.  App. A.2-A.3.
+template <int G, class P>
+__device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* rhs) {
+  constexpr bool g1 = G == 0 || G == 1 || G == 13, g2 = G == 0 || G == 2, g3 = G == 0 || G == 3 || G == 13;
   // ---- point values
   double gt[6], At[6];
 #pragma unroll
-  for (int s = 0; s < 6; ++s) { gt[s] = ld(F(V_GT + s) + c); At[s] = ld(F(V_AT + s) + c); }
-  const double phi = ld(F(V_PHI) + c), trK = ld(F(V_TRK) + c), alpha = ld(F(V_ALPHA) + c);
-  const double Aux = ld(F(V_AUX) + c);
+  for (int s = 0; s < 6; ++s) { gt[s] = D.v(V_GT + s); At[s] = D.v(V_AT + s); }
+  const double phi = D.v(V_PHI), trK = D.v(V_TRK), alpha = D.v(V_ALPHA);
+  const double Aux = D.v(V_AUX);
   double Xt[3], beta[3], Bv[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    Xt[i] = ld(F(V_XT + i) + c); beta[i] = ld(F(V_BETA + i) + c); Bv[i] = ld(F(V_B + i) + c);
-  }
+  for (int i = 0; i < 3; ++i) { Xt[i] = D.v(V_XT + i); beta[i] = D.v(V_BETA + i); Bv[i] = D.v(V_B + i); }
   double dbeta[3][3];  // dbeta[l][k] = d_l beta^k
 #pragma unroll
   for (int l = 0; l < 3; ++l)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) dbeta[l][k] = D1raw(F(V_BETA + k), c, st.s[l]) * K.i12h[l];
+    for (int k = 0; k < 3; ++k) dbeta[l][k] = D.d1(V_BETA + k, l);
   const double divb = dbeta[0][0] + dbeta[1][1] + dbeta[2][2];
 
   if (g1) {
@@ -164,7 +214,7 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
 #pragma unroll
       for (int l = 0; l < 3; ++l)
 #pragma unroll
-        for (int s = 0; s < 6; ++s) dg[l][s] = D1raw(F(V_GT + s), c, st.s[l]) * K.i12h[l];
+        for (int s = 0; s < 6; ++s) dg[l][s] = D.d1(V_GT + s, l);
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -190,8 +240,8 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
     double dphi[3], dalpha[3];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
-      dphi[l] = D1raw(F(V_PHI), c, st.s[l]) * K.i12h[l];
-      dalpha[l] = D1raw(F(V_ALPHA), c, st.s[l]) * K.i12h[l];
+      dphi[l] = D.d1(V_PHI, l);
+      dalpha[l] = D.d1(V_ALPHA, l);
     }
     // ---- raised At: Am[i][j] = At^i_j (full 3x3), Au = At^ij (sym)
     double Am[3][3];
@@ -213,23 +263,17 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
 #pragma unroll
       for (int l = 0; l < 3; ++l)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) dXt[l][k] = D1raw(F(V_XT + k), c, st.s[l]) * K.i12h[l];
-      // ---- conformal Ricci tensor R~_ij
+        for (int k = 0; k < 3; ++k) dXt[l][k] = D.d1(V_XT + k, l);
+      // ---- conformal Ricci tensor R~_ij: -1/2 gu^lm d_l d_m gt_ij, pair (l,m) at a time
       double Rt[6];
 #pragma unroll
       for (int s = 0; s < 6; ++s) Rt[s] = 0.0;
-      // -1/2 gu^lm d_l d_m gt_ij, pair (l,m) at a time
 #pragma unroll
       for (int p = 0; p < 6; ++p) {
         const int l = sI(p), m = sJ(p);
         const double w = -0.5 * mult(p) * gu[p];
 #pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          const double* f = F(V_GT + s);
-          const double dd = (l == m) ? D2raw(f, c, st.s[l], gt[s]) * K.i12h2[l]
-                                     : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
-          Rt[s] = fma(w, dd, Rt[s]);
-        }
+        for (int s = 0; s < 6; ++s) Rt[s] = fma(w, D.dd(V_GT + s, l, m, gt[s]), Rt[s]);
       }
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
@@ -261,10 +305,8 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
         const int i = sI(s), j = sJ(s);
-        const double ddp = (i == j) ? D2raw(F(V_PHI), c, st.s[i], phi) * K.i12h2[i]
-                                    : D11raw(F(V_PHI), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
-        const double dda = (i == j) ? D2raw(F(V_ALPHA), c, st.s[i], alpha) * K.i12h2[i]
-                                    : D11raw(F(V_ALPHA), c, st.s[i], st.s[j]) * K.i144hh[i + j - 1];
+        const double ddp = D.dd(V_PHI, i, j, phi);
+        const double dda = D.dd(V_ALPHA, i, j, alpha);
         ddalpha[s] = dda;
         DDphi[s] = ddp - (Gu[0][s] * dphi[0] + Gu[1][s] * dphi[1] + Gu[2][s] * dphi[2]);
       }
@@ -326,7 +368,7 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
     if (g3) {
       double dtrK[3];
 #pragma unroll
-      for (int l = 0; l < 3; ++l) dtrK[l] = D1raw(F(V_TRK), c, st.s[l]) * K.i12h[l];
+      for (int l = 0; l < 3; ++l) dtrK[l] = D.d1(V_TRK, l);
       double ddivb[3] = {0.0, 0.0, 0.0};  // d_j (d . beta)
       double lapb[3] = {0.0, 0.0, 0.0};   // gt^jk d_j d_k beta^i
 #pragma unroll
@@ -334,9 +376,7 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
         const int l = sI(p), m = sJ(p);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          const double* f = F(V_BETA + i);
-          const double dd = (l == m) ? D2raw(f, c, st.s[l], beta[i]) * K.i12h2[l]
-                                     : D11raw(f, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
+          const double dd = D.dd(V_BETA + i, l, m, beta[i]);
           lapb[i] = fma(mult(p) * gu[p], dd, lapb[i]);
           // d_l d_m beta^i feeds d_j (d.beta) for (j = l, i = m) and (j = m, i = l)
           if (i == m) ddivb[l] += dd;
@@ -376,20 +416,19 @@ __device__ __forceinline__ void bssn_point(const double* __restrict__ in, int64_
   };
 #pragma unroll
   for (int v = 0; v < V_ALPHA; ++v)
-    if (in_group(G, v)) rhs[v] += adv(F(v), c, st, beta, centre(v), K);
+    if (in_group(G, v)) rhs[v] += D.adv(v, beta, centre(v));
   if (g1) {
-    rhs[V_ALPHA] = fma(K.c_alpha_adv, adv(F(V_ALPHA), c, st, beta, alpha, K), rhs[V_ALPHA]);
+    rhs[V_ALPHA] = fma(K.c_alpha_adv, D.adv(V_ALPHA, beta, alpha), rhs[V_ALPHA]);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-      rhs[V_BETA + i] = fma(K.c_beta_adv, adv(F(V_BETA + i), c, st, beta, beta[i], K), rhs[V_BETA + i]);
+      rhs[V_BETA + i] = fma(K.c_beta_adv, D.adv(V_BETA + i, beta, beta[i]), rhs[V_BETA + i]);
   }
-  if (g2)
-    rhs[V_AUX] = K.L * (rhs[V_TRK] - K.eta_alpha * Aux) + K.c_alpha_adv * adv(F(V_AUX), c, st, beta, Aux, K);
+  if (g2) rhs[V_AUX] = K.L * (rhs[V_TRK] - K.eta_alpha * Aux) + K.c_alpha_adv * D.adv(V_AUX, beta, Aux);
   if (g3) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double advB = adv(F(V_B + i), c, st, beta, Bv[i], K);
-      const double advX = adv(F(V_XT + i), c, st, beta, Xt[i], K);
+      const double advB = D.adv(V_B + i, beta, Bv[i]);
+      const double advX = D.adv(V_XT + i, beta, Xt[i]);
       rhs[V_B + i] = K.S_B * (rhs[V_XT + i] - K.eta * Bv[i]) + K.c_beta_adv * (advB - advX);
     }
   }
@@ -411,22 +450,13 @@ BssnK make_k(const StageLaunch& a, const double* prm) {
   return K;
 }
 
-// One thread per interior point (x fastest), computing the RHS group G and applying the
-// RK4 stage update to that group's GFs.  STAGE 0 = RHS only (writes k to dst).
+// RK4 stage update of the GFs of group G at point c (interior (i,j,k)) and the stores.
 template <int STAGE, int G>
-__global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, double* rhs_dst) {
+__device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K, const double* r,
+                                            const double* in, int64_t c, int i, int j, int k,
+                                            double* rhs_dst) {
   const Layout& L = a.L;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const int k = a.k_begin + blockIdx.z * blockDim.z + threadIdx.z;
-  if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
-  const int64_t c = L.idx(i, j, k);
   const int64_t gfs = L.gfs;
-  const double* in = (STAGE <= 1) ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b));
-  Strides st;
-  st.s[0] = 1; st.s[1] = L.px; st.s[2] = L.plane;
-  double r[NV];
-  bssn_point<G>(in, gfs, c, st, K, r);
   if (STAGE == 0) {
     const int64_t ni = L.nx * L.ny * L.nz;
     const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
@@ -458,12 +488,97 @@ __global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, doubl
   }
 }
 
+template <int STAGE>
+__device__ __forceinline__ const double* stage_input(const StageLaunch& a) {
+  return (STAGE <= 1) ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b));
+}
+
+// ------------------------------------------------------------------ one thread per point
+// Computes the RHS group G (stencils from global memory) and the RK4 stage update of that
+// group's GFs.  G = 0: the fused single kernel; G = 1, 2, 3: the fissioned kernels.
+template <int STAGE, int G>
+__global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, double* rhs_dst) {
+  const Layout& L = a.L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = a.k_begin + blockIdx.z * blockDim.z + threadIdx.z;
+  if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
+  const int64_t c = L.idx(i, j, k);
+  const double* in = stage_input<STAGE>(a);
+  StencilP P{in, L.gfs, c, {{1, L.px, L.plane}}, &K};
+  double r[NV];
+  bssn_point<G>(P, K, r);
+  bssn_update<STAGE, G>(a, K, r, in, c, i, j, k, rhs_dst);
+}
+
+// ------------------------------------------------------------------ two-phase table kernel
+// CTA = 32 consecutive x points of one row (TP points), 64 threads.  Phase 1: the 161
+// table slots of the 32 points are computed by the 2 warps slot by slot (each warp one
+// slot for its 32 points: coalesced loads, a handful of live registers, many independent
+// loads in flight).  Phase 2: warp 0 runs the curvature group G2 (trK, At, A), warp 1 the
+// kinematic + shift groups G1 + G3, both reading derivatives from the table.
+constexpr int TP = 32;
+template <int STAGE>
+__global__ void __launch_bounds__(64) bssn_tab(StageLaunch a, BssnK K, double* rhs_dst) {
+  __shared__ double tab[NSLOT * TP];
+  const Layout& L = a.L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * TP + lane;
+  const int j = blockIdx.y;
+  const int k = a.k_begin + blockIdx.z;
+  const bool live = i < L.nx;
+  const int ic = live ? i : L.nx - 1;  // dead lanes recompute a valid point (discarded)
+  const int64_t c = L.idx(ic, j, k);
+  const int64_t gfs = L.gfs;
+  const double* in = stage_input<STAGE>(a);
+  const int64_t st[3] = {1, L.px, L.plane};
+  // phase 1 -- point values first (the advection slots need beta, the D2 slots f0)
+  for (int s = warp; s < T_D1; s += 2) tab[s * TP + lane] = ld(in + s * gfs + c);
+  __syncthreads();
+  double beta[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) beta[q] = tab[(V_BETA + q) * TP + lane];
+#pragma unroll 1
+  for (int s = T_D1 + warp; s < NSLOT; s += 2) {
+    double val;
+    if (s < T_DD) {
+      const int e = s - T_D1, l = e % 3;
+      const int gf = d1gf(e / 3);
+      val = D1raw(in + gf * gfs, c, st[l]) * K.i12h[l];
+    } else if (s < T_ADV) {
+      const int e = s - T_DD, p = e % 6;
+      const int gf = ddgf(e / 6);
+      const int l = sI(p), m = sJ(p);
+      val = (l == m) ? D2raw(in + gf * gfs, c, st[l], tab[gf * TP + lane]) * K.i12h2[l]
+                     : D11raw(in + gf * gfs, c, st[l], st[m]) * K.i144hh[l + m - 1];
+    } else {
+      const int gf = s - T_ADV;
+      const double f0 = tab[gf * TP + lane];
+      double r = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) r = fma(ADVraw(in + gf * gfs, c, st[q], f0, beta[q]), K.i24h[q], r);
+      val = r;
+    }
+    tab[s * TP + lane] = val;
+  }
+  __syncthreads();
+  // phase 2 -- the algebra from the table, two equation groups per point
+  TabP<TP> P{tab, lane};
+  double r[NV];
+  if (warp == 0) {
+    bssn_point<2>(P, K, r);
+    if (live) bssn_update<STAGE, 2>(a, K, r, in, c, i, j, k, rhs_dst);
+  } else {
+    bssn_point<13>(P, K, r);
+    if (live) bssn_update<STAGE, 13>(a, K, r, in, c, i, j, k, rhs_dst);
+  }
+}
+
 template <int STAGE, int G>
 cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
-  // CTA shape (128 threads): CHEMORA_BSSN_BLOCK = "BXxBYxBZ" (default 32x4x1).  A compact
-  // 3-D shape keeps more of each GF's stencil footprint inside the CTA (L1 hits).
+  // CTA shape (128 threads): CHEMORA_BSSN_BLOCK = "BXxBYxBZ" (default 32x4x1).
   static int bdim[3] = {0, 0, 0};
   if (!bdim[0]) {
     bdim[0] = 32; bdim[1] = 4; bdim[2] = 1;
@@ -480,13 +595,26 @@ cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream
 }
 
 template <int STAGE>
+cudaError_t launch_tab(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((a.L.nx + TP - 1) / TP), (unsigned)a.L.ny, (unsigned)nk);
+  bssn_tab<STAGE><<<grid, 64, 0, st>>>(a, K, dst);
+  return cudaGetLastError();
+}
+
+template <int STAGE>
 cudaError_t launch_stage(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
-  // variant 1: the fused single kernel; default: the fissioned kernels G1, G2, G3
+  // variant 0 (default): two-phase table kernel; 1: fused single kernel (stencils from
+  // global memory); 2: the fissioned kernels G1, G2, G3
   if (a.variant == 1) return launch<STAGE, 0>(a, K, dst, st);
-  cudaError_t e = launch<STAGE, 1>(a, K, dst, st);
-  if (e == cudaSuccess) e = launch<STAGE, 2>(a, K, dst, st);
-  if (e == cudaSuccess) e = launch<STAGE, 3>(a, K, dst, st);
-  return e;
+  if (a.variant == 2) {
+    cudaError_t e = launch<STAGE, 1>(a, K, dst, st);
+    if (e == cudaSuccess) e = launch<STAGE, 2>(a, K, dst, st);
+    if (e == cudaSuccess) e = launch<STAGE, 3>(a, K, dst, st);
+    return e;
+  }
+  return launch_tab<STAGE>(a, K, dst, st);
 }
 
 cudaError_t dispatch(const StageLaunch& a, int stage, double* dst, cudaStream_t st, const double* hparams) {

@@ -632,6 +632,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     if (order == 4 && g->L.g >= 4 && !g->monitor) cands.push_back({kVariantFused, 0});
   } else {
     cands.push_back({0, 0});
+    cands.push_back({2, 0});  // fissioned one-thread-per-point kernels
     if (g->L.nx * g->L.ny * g->L.nz <= (int64_t)64 * 64 * 64) cands.push_back({1, 0});
   }
   const int saved_v = g->variant, saved_b = g->band;
