@@ -538,28 +538,47 @@ __global__ void __launch_bounds__(64) bssn_tab(StageLaunch a, BssnK K, double* r
   double beta[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) beta[q] = tab[(V_BETA + q) * TP + lane];
+  // first derivatives: 15 GFs x 3 axes, the warp's 3 axes of one GF per iteration (12
+  // independent loads in flight per thread)
 #pragma unroll 1
-  for (int s = T_D1 + warp; s < NSLOT; s += 2) {
-    double val;
-    if (s < T_DD) {
-      const int e = s - T_D1, l = e % 3;
-      const int gf = d1gf(e / 3);
-      val = D1raw(in + gf * gfs, c, st[l]) * K.i12h[l];
-    } else if (s < T_ADV) {
-      const int e = s - T_DD, p = e % 6;
-      const int gf = ddgf(e / 6);
-      const int l = sI(p), m = sJ(p);
-      val = (l == m) ? D2raw(in + gf * gfs, c, st[l], tab[gf * TP + lane]) * K.i12h2[l]
-                     : D11raw(in + gf * gfs, c, st[l], st[m]) * K.i144hh[l + m - 1];
-    } else {
-      const int gf = s - T_ADV;
-      const double f0 = tab[gf * TP + lane];
-      double r = 0.0;
+  for (int e = warp; e < 15; e += 2) {
+    const double* f = in + d1gf(e) * gfs;
+    const double a0 = D1raw(f, c, st[0]), a1 = D1raw(f, c, st[1]), a2 = D1raw(f, c, st[2]);
+    tab[(T_D1 + 3 * e + 0) * TP + lane] = a0 * K.i12h[0];
+    tab[(T_D1 + 3 * e + 1) * TP + lane] = a1 * K.i12h[1];
+    tab[(T_D1 + 3 * e + 2) * TP + lane] = a2 * K.i12h[2];
+  }
+  // second derivatives: 11 GFs x 6 pairs, all six of one GF per iteration
+#pragma unroll 1
+  for (int e = warp; e < 11; e += 2) {
+    const int gf = ddgf(e);
+    const double* f = in + gf * gfs;
+    const double f0 = tab[gf * TP + lane];
+    const double xx = D2raw(f, c, st[0], f0), yy = D2raw(f, c, st[1], f0), zz = D2raw(f, c, st[2], f0);
+    const double xy = D11raw(f, c, st[0], st[1]), xz = D11raw(f, c, st[0], st[2]), yz = D11raw(f, c, st[1], st[2]);
+    double* o = tab + (T_DD + 6 * e) * TP + lane;
+    o[0 * TP] = xx * K.i12h2[0];
+    o[1 * TP] = xy * K.i144hh[0];
+    o[2 * TP] = xz * K.i144hh[1];
+    o[3 * TP] = yy * K.i12h2[1];
+    o[4 * TP] = yz * K.i144hh[2];
+    o[5 * TP] = zz * K.i12h2[2];
+  }
+  // advection terms, two GFs per iteration
+#pragma unroll 1
+  for (int gf = warp; gf < NV; gf += 4) {
+    double r[2];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) r = fma(ADVraw(in + gf * gfs, c, st[q], f0, beta[q]), K.i24h[q], r);
-      val = r;
+    for (int u = 0; u < 2; ++u) {
+      const int v = gf + 2 * u < NV ? gf + 2 * u : gf;
+      const double f0 = tab[v * TP + lane];
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc = fma(ADVraw(in + v * gfs, c, st[q], f0, beta[q]), K.i24h[q], acc);
+      r[u] = acc;
     }
-    tab[s * TP + lane] = val;
+    tab[(T_ADV + gf) * TP + lane] = r[0];
+    if (gf + 2 < NV) tab[(T_ADV + gf + 2) * TP + lane] = r[1];
   }
   __syncthreads();
   // phase 2 -- the algebra from the table, two equation groups per point
