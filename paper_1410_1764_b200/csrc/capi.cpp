@@ -400,7 +400,8 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->cur = 0;
   // default tiling: the temporally blocked stage pairs for 4th-order wave grids (fastest
   // measured, profiles/r1_wave_design_study.md), else one thread per point; BSSN: fission
-  g->variant = (desc->system == CHEMORA_SYS_WAVE && (desc->fd_order == 0 || desc->fd_order == 4)) ? kVariantFused : 0;
+  g->variant = desc->system == CHEMORA_SYS_BSSN ? 2 /* fissioned G1/G2/G3 */
+             : (desc->fd_order == 0 || desc->fd_order == 4) ? kVariantFused : 0;
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
