@@ -108,19 +108,18 @@ struct StencilP {
   const double* in;
   int64_t gfs, c;
   Strides st;
-  const BssnK* K;
   __device__ __forceinline__ double v(int gf) const { return ld(in + gf * gfs + c); }
-  __device__ __forceinline__ double d1(int gf, int l) const {
-    return D1raw(in + gf * gfs, c, st.s[l]) * K->i12h[l];
+  __device__ __forceinline__ double d1(const BssnK& K, int gf, int l) const {
+    return D1raw(in + gf * gfs, c, st.s[l]) * K.i12h[l];
   }
-  __device__ __forceinline__ double dd(int gf, int l, int m, double f0) const {
-    return (l == m) ? D2raw(in + gf * gfs, c, st.s[l], f0) * K->i12h2[l]
-                    : D11raw(in + gf * gfs, c, st.s[l], st.s[m]) * K->i144hh[l + m - 1];
+  __device__ __forceinline__ double dd(const BssnK& K, int gf, int l, int m, double f0) const {
+    return (l == m) ? D2raw(in + gf * gfs, c, st.s[l], f0) * K.i12h2[l]
+                    : D11raw(in + gf * gfs, c, st.s[l], st.s[m]) * K.i144hh[l + m - 1];
   }
-  __device__ __forceinline__ double adv(int gf, const double* beta, double f0) const {
+  __device__ __forceinline__ double adv(const BssnK& K, int gf, const double* beta, double f0) const {
     double r = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) r = fma(ADVraw(in + gf * gfs, c, st.s[a], f0, beta[a]), K->i24h[a], r);
+    for (int a = 0; a < 3; ++a) r = fma(ADVraw(in + gf * gfs, c, st.s[a], f0, beta[a]), K.i24h[a], r);
     return r;
   }
 };
@@ -130,11 +129,11 @@ struct TabP {
   const double* tab;  // [NSLOT][NP]
   int pt;
   __device__ __forceinline__ double v(int gf) const { return tab[gf * NP + pt]; }
-  __device__ __forceinline__ double d1(int gf, int l) const { return tab[(T_D1 + 3 * d1i(gf) + l) * NP + pt]; }
-  __device__ __forceinline__ double dd(int gf, int l, int m, double) const {
+  __device__ __forceinline__ double d1(const BssnK&, int gf, int l) const { return tab[(T_D1 + 3 * d1i(gf) + l) * NP + pt]; }
+  __device__ __forceinline__ double dd(const BssnK&, int gf, int l, int m, double) const {
     return tab[(T_DD + 6 * ddi(gf) + sy(l, m)) * NP + pt];
   }
-  __device__ __forceinline__ double adv(int gf, const double*, double) const { return tab[(T_ADV + gf) * NP + pt]; }
+  __device__ __forceinline__ double adv(const BssnK&, int gf, const double*, double) const { return tab[(T_ADV + gf) * NP + pt]; }
 };
 
 // Output groups of the kernel fission (fission is "the most
@@ -168,7 +167,7 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
 #pragma unroll
   for (int l = 0; l < 3; ++l)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) dbeta[l][k] = D.d1(V_BETA + k, l);
+    for (int k = 0; k < 3; ++k) dbeta[l][k] = D.d1(K, V_BETA + k, l);
   const double divb = dbeta[0][0] + dbeta[1][1] + dbeta[2][2];
 
   if (g1) {
@@ -214,7 +213,7 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
 #pragma unroll
       for (int l = 0; l < 3; ++l)
 #pragma unroll
-        for (int s = 0; s < 6; ++s) dg[l][s] = D.d1(V_GT + s, l);
+        for (int s = 0; s < 6; ++s) dg[l][s] = D.d1(K, V_GT + s, l);
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -240,8 +239,8 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
     double dphi[3], dalpha[3];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
-      dphi[l] = D.d1(V_PHI, l);
-      dalpha[l] = D.d1(V_ALPHA, l);
+      dphi[l] = D.d1(K, V_PHI, l);
+      dalpha[l] = D.d1(K, V_ALPHA, l);
     }
     // ---- raised At: Am[i][j] = At^i_j (full 3x3), Au = At^ij (sym)
     double Am[3][3];
@@ -263,7 +262,7 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
 #pragma unroll
       for (int l = 0; l < 3; ++l)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) dXt[l][k] = D.d1(V_XT + k, l);
+        for (int k = 0; k < 3; ++k) dXt[l][k] = D.d1(K, V_XT + k, l);
       // ---- conformal Ricci tensor R~_ij: -1/2 gu^lm d_l d_m gt_ij, pair (l,m) at a time
       double Rt[6];
 #pragma unroll
@@ -273,7 +272,7 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
         const int l = sI(p), m = sJ(p);
         const double w = -0.5 * mult(p) * gu[p];
 #pragma unroll
-        for (int s = 0; s < 6; ++s) Rt[s] = fma(w, D.dd(V_GT + s, l, m, gt[s]), Rt[s]);
+        for (int s = 0; s < 6; ++s) Rt[s] = fma(w, D.dd(K, V_GT + s, l, m, gt[s]), Rt[s]);
       }
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
@@ -305,8 +304,8 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
         const int i = sI(s), j = sJ(s);
-        const double ddp = D.dd(V_PHI, i, j, phi);
-        const double dda = D.dd(V_ALPHA, i, j, alpha);
+        const double ddp = D.dd(K, V_PHI, i, j, phi);
+        const double dda = D.dd(K, V_ALPHA, i, j, alpha);
         ddalpha[s] = dda;
         DDphi[s] = ddp - (Gu[0][s] * dphi[0] + Gu[1][s] * dphi[1] + Gu[2][s] * dphi[2]);
       }
@@ -368,7 +367,7 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
     if (g3) {
       double dtrK[3];
 #pragma unroll
-      for (int l = 0; l < 3; ++l) dtrK[l] = D.d1(V_TRK, l);
+      for (int l = 0; l < 3; ++l) dtrK[l] = D.d1(K, V_TRK, l);
       double ddivb[3] = {0.0, 0.0, 0.0};  // d_j (d . beta)
       double lapb[3] = {0.0, 0.0, 0.0};   // gt^jk d_j d_k beta^i
 #pragma unroll
@@ -376,7 +375,7 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
         const int l = sI(p), m = sJ(p);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          const double dd = D.dd(V_BETA + i, l, m, beta[i]);
+          const double dd = D.dd(K, V_BETA + i, l, m, beta[i]);
           lapb[i] = fma(mult(p) * gu[p], dd, lapb[i]);
           // d_l d_m beta^i feeds d_j (d.beta) for (j = l, i = m) and (j = m, i = l)
           if (i == m) ddivb[l] += dd;
@@ -416,19 +415,19 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
   };
 #pragma unroll
   for (int v = 0; v < V_ALPHA; ++v)
-    if (in_group(G, v)) rhs[v] += D.adv(v, beta, centre(v));
+    if (in_group(G, v)) rhs[v] += D.adv(K, v, beta, centre(v));
   if (g1) {
-    rhs[V_ALPHA] = fma(K.c_alpha_adv, D.adv(V_ALPHA, beta, alpha), rhs[V_ALPHA]);
+    rhs[V_ALPHA] = fma(K.c_alpha_adv, D.adv(K, V_ALPHA, beta, alpha), rhs[V_ALPHA]);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-      rhs[V_BETA + i] = fma(K.c_beta_adv, D.adv(V_BETA + i, beta, beta[i]), rhs[V_BETA + i]);
+      rhs[V_BETA + i] = fma(K.c_beta_adv, D.adv(K, V_BETA + i, beta, beta[i]), rhs[V_BETA + i]);
   }
-  if (g2) rhs[V_AUX] = K.L * (rhs[V_TRK] - K.eta_alpha * Aux) + K.c_alpha_adv * D.adv(V_AUX, beta, Aux);
+  if (g2) rhs[V_AUX] = K.L * (rhs[V_TRK] - K.eta_alpha * Aux) + K.c_alpha_adv * D.adv(K, V_AUX, beta, Aux);
   if (g3) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double advB = D.adv(V_B + i, beta, Bv[i]);
-      const double advX = D.adv(V_XT + i, beta, Xt[i]);
+      const double advB = D.adv(K, V_B + i, beta, Bv[i]);
+      const double advX = D.adv(K, V_XT + i, beta, Xt[i]);
       rhs[V_B + i] = K.S_B * (rhs[V_XT + i] - K.eta * Bv[i]) + K.c_beta_adv * (advB - advX);
     }
   }
@@ -496,8 +495,12 @@ __device__ __forceinline__ const double* stage_input(const StageLaunch& a) {
 // ------------------------------------------------------------------ one thread per point
 // Computes the RHS group G (stencils from global memory) and the RK4 stage update of that
 // group's GFs.  G = 0: the fused single kernel; G = 1, 2, 3: the fissioned kernels.
+// register budget per group (128-thread CTAs): unconstrained -- capping G1 at 128 and G3
+// at 168 registers measured slower (0.188 vs 0.221 G updates/s at 192^3: spills)
+template <int G> struct MinBlocks { static constexpr int value = 1; };
+
 template <int STAGE, int G>
-__global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, double* rhs_dst) {
+__global__ void __launch_bounds__(128, MinBlocks<G>::value) bssn_simple(StageLaunch a, BssnK K, double* rhs_dst) {
   const Layout& L = a.L;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(128) bssn_simple(StageLaunch a, BssnK K, doubl
   if (i >= L.nx || j >= L.ny || k >= a.k_end) return;
   const int64_t c = L.idx(i, j, k);
   const double* in = stage_input<STAGE>(a);
-  StencilP P{in, L.gfs, c, {{1, L.px, L.plane}}, &K};
+  StencilP P{in, L.gfs, c, {{1, L.px, L.plane}}};
   double r[NV];
   bssn_point<G>(P, K, r);
   bssn_update<STAGE, G>(a, K, r, in, c, i, j, k, rhs_dst);
