@@ -58,10 +58,13 @@ constexpr int PY_R = r128(IR_X * IR_Y * 8), PY_1 = r128(I1_X * I1_Y * 8), PY_2 =
               PY_3 = r128(I3_X * I3_Y * 8);
 constexpr int IZ_B = r128(IR_X * IR_Y * 8) + r128(I3_X * I3_Y * 8);  // intermediate z ring slot
 constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermediate p ring slot
-constexpr int RZ = 7, RI_Z = 5, RI_P = 3;
+constexpr int RI_Z = 5, RI_P = 3;
 
 template <bool B> struct Geo {
-  static constexpr int RP = B ? 4 : 5;
+  // input ring depths: kernel A has the shared memory for 5 (Z) / 5 (P) planes of
+  // prefetch beyond the resident window; kernel B (more operands) for 2 / 1
+  static constexpr int RZ = B ? 7 : 10;
+  static constexpr int RP = B ? 4 : 8;
   static constexpr int RQ = B ? 3 : 0;
   static constexpr int PSLOT = P1_B + P2_B + (B ? PY_R + PY_1 + PY_2 + PY_3 : 0);
   static constexpr uint32_t PBYTES =
@@ -100,15 +103,15 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* zfull = bars;
-  uint64_t* zempty = zfull + RZ;
-  uint64_t* pfull = zempty + RZ;
+  uint64_t* zempty = zfull + G::RZ;
+  uint64_t* pfull = zempty + G::RZ;
   uint64_t* pempty = pfull + G::RP;
   uint64_t* qfull = pempty + G::RP;
   uint64_t* qempty = qfull + G::RQ;
   const Layout& L = a.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, NCW); }
+    for (int s = 0; s < G::RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, NCW); }
     for (int s = 0; s < G::RP; ++s) { mbar_init(pfull + s, 1); mbar_init(pempty + s, NCW); }
     for (int s = 0; s < G::RQ; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, NCW); }
     fence_mbar_init();
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int nk = min(kchunk, a.k_begin + nkall - kb);
       const int xo = kXOff + i0, yo = g + j0;
       auto loadZ = [&](int plane) {
-        const uint32_t s = nz % RZ, n = nz / RZ;
+        const uint32_t s = nz % G::RZ, n = nz / G::RZ;
         if (n > 0) mbar_wait(zempty + s, (n - 1) & 1);
         unsigned char* d = smem + s * ZSLOT;
         mbar_arrive_expect_tx(zfull + s, ZBYTES);
@@ -237,16 +240,16 @@ __global__ void __launch_bounds__(NT, 1)
     const int kb = a.k_begin + ch * kchunk;
     const int nk = min(kchunk, a.k_begin + nkall - kb);
     const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
-    for (int q = 0; q < 4; ++q) mbar_wait(zfull + (z0 + q) % RZ, ((z0 + q) / RZ) & 1);
+    for (int q = 0; q < 4; ++q) mbar_wait(zfull + (z0 + q) % G::RZ, ((z0 + q) / G::RZ) & 1);
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
     int64_t cglob = L.idx(i, j, kb);  // global offset of this thread's point at plane k
     // ring slots: input planes p-2..p+2, P planes p and p-2, intermediate planes
     int zsl[5];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) zsl[q] = (int)((z0 + q) % RZ);
+    for (int q = 0; q < 5; ++q) zsl[q] = (int)((z0 + q) % G::RZ);
     int psl = (int)(p0 % G::RP), psl2 = 0;   // P slot of plane p, of plane p-2
-    int zph = (int)(((z0 + 4) / RZ) & 1);    // phase of the input slot zsl[4]
+    int zph = (int)(((z0 + 4) / G::RZ) & 1);    // phase of the input slot zsl[4]
     int pph = (int)((p0 / G::RP) & 1);
     int izs[5] = {0, 0, 0, 0, 0};           // intermediate z slots of planes p-4..p
     int ips[3] = {0, 0, 0};                 // intermediate p slots of planes p-2..p
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(NT, 1)
       // advance the rings: input planes shift by one, P slot of plane p+1, of plane p-1
 #pragma unroll
       for (int q = 0; q < 4; ++q) zsl[q] = zsl[q + 1];
-      zsl[4] = zsl[3] + 1 == RZ ? 0 : zsl[3] + 1;
+      zsl[4] = zsl[3] + 1 == G::RZ ? 0 : zsl[3] + 1;
       if (zsl[4] == 0) zph ^= 1;
       // P slot of plane (p+1)-2 for the next iteration: ring index p0 + jj - 1
       psl2 = (jj == 1) ? (int)(p0 % G::RP) : (psl2 + 1 == G::RP ? 0 : psl2 + 1);
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(NT, 1)
     __syncwarp();
     if (lane == 0) {
       for (int q = 0; q < 2; ++q) mbar_arrive(pempty + (p0 + nk + 2 + q) % G::RP);
-      for (int q = 0; q < 4; ++q) mbar_arrive(zempty + (z0 + nk + 4 + q) % RZ);
+      for (int q = 0; q < 4; ++q) mbar_arrive(zempty + (z0 + nk + 4 + q) % G::RZ);
     }
     nz = z0 + nk + 8;
     np = p0 + nk + 4;
