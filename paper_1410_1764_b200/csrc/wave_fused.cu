@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int xo = kXOff + i0, yo = g + j0;
       auto loadZ = [&](int plane) {
         const uint32_t s = nz % G::RZ, n = nz / G::RZ;
-        if (n > 0) mbar_wait_sleepy(zempty + s, (n - 1) & 1);
+        if (n > 0) mbar_wait(zempty + s, (n - 1) & 1);
         unsigned char* d = smem + s * ZSLOT;
         mbar_arrive_expect_tx(zfull + s, ZBYTES);
         tma_load_4d(d, &M.rho, zfull + s, xo - H, yo - H, g + plane, GRHO);
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NT, 1)
       };
       auto loadP = [&](int plane) {
         const uint32_t s = np % G::RP, n = np / G::RP;
-        if (n > 0) mbar_wait_sleepy(pempty + s, (n - 1) & 1);
+        if (n > 0) mbar_wait(pempty + s, (n - 1) & 1);
         unsigned char* d = smem + G::OFF_P + s * G::PSLOT;
         uint64_t* bar = pfull + s;
         mbar_arrive_expect_tx(bar, G::PBYTES);
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(NT, 1)
       };
       auto loadQ = [&](int plane) {
         const uint32_t s = nq % G::RQ, n = nq / G::RQ;
-        if (n > 0) mbar_wait_sleepy(qempty + s, (n - 1) & 1);
+        if (n > 0) mbar_wait(qempty + s, (n - 1) & 1);
         unsigned char* d = smem + G::OFF_Q + s * G::QSLOT;
         mbar_arrive_expect_tx(qfull + s, G::QBYTES);
         tma_load_4d(d, &M.q5, qfull + s, xo, yo, g + plane, GU);
