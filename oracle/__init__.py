@@ -50,6 +50,7 @@ def lib():
                                                ctypes.c_double, ctypes.c_int, dp, ctypes.c_int]
         L.chemora_oracle_norms.argtypes = [ctypes.c_int, dp, i64p, ctypes.c_int, dp, dp]
         L.chemora_oracle_default_bssn_params.argtypes = [dp]
+        L.chemora_oracle_constraints.argtypes = [dp, i64p, ctypes.c_int, dp, dp]
         _lib = L
     return _lib
 
@@ -148,4 +149,18 @@ def norms(system: int, interior: np.ndarray, spacing, g: int = DEFAULT_GHOST) ->
     rc = lib().chemora_oracle_norms(system, _dp(y), _ext(n), g, _sp(spacing), _dp(out))
     if rc:
         raise ValueError(f"oracle norms rc={rc}")
+    return out
+
+
+CONSTRAINT_NAMES = ("H", "M1", "M2", "M3", "G1", "G2", "G3")
+
+
+def constraints(interior: np.ndarray, spacing, g: int = DEFAULT_GHOST) -> np.ndarray:
+    """BSSN constraint fields [H, M1..3, G1..3] on a periodic grid, shape [7][Nz][Ny][Nx]."""
+    y = fill_ghosts(pad(np.ascontiguousarray(interior, dtype=np.float64), g), g)
+    n = extent_of(interior)
+    out = np.zeros((7, n[2], n[1], n[0]))
+    rc = lib().chemora_oracle_constraints(_dp(y), _ext(n), g, _sp(spacing), _dp(out))
+    if rc:
+        raise ValueError(f"oracle constraints rc={rc}")
     return out

@@ -426,6 +426,143 @@ void bssn_rhs(const double* y, double* kout, const Grid& G, const double* prm) {
       }
 }
 
+// ---------------------------------------------------------------- BSSN constraints
+// Vacuum constraints of the BSSN variables (PAPER.md:472-473
+// "constraint equations"), evaluated with the same 4th-order stencils:
+//   H   = R + 2/3 K^2 - At_ij At^ij,   R = e^{-4 phi} gt^ij (R~_ij + R^phi_ij)   (App. A.2)
+//   M^i = d_j At^ij + Gt^i_jk At^jk + 6 At^ij d_j phi - 2/3 gt^ij d_j K
+//   G^i = Xt^i - gt^jk Gt^i_jk
+// out: 7 interior fields [H, M1, M2, M3, G1, G2, G3].
+void bssn_constraints(const double* y, double* out, const Grid& G) {
+  const int64_t np = G.npad(), ni = G.nint();
+  const int64_t st[3] = {1, G.p[0], G.p[0] * G.p[1]};
+  const double* h = G.h;
+#pragma omp parallel for schedule(static)
+  for (int64_t kk = 0; kk < G.n[2]; ++kk)
+    for (int64_t jj = 0; jj < G.n[1]; ++jj)
+      for (int64_t ii = 0; ii < G.n[0]; ++ii) {
+        const int64_t c = G.at(ii, jj, kk), o = G.at_int(ii, jj, kk);
+        auto F = [&](int v) { return y + v * np; };
+        const double phi = F(PHI)[c], trK = F(TRK)[c];
+        double gt[3][3], At[3][3], Xt[3];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) { gt[i][j] = F(GT + sym(i, j))[c]; At[i][j] = F(AT + sym(i, j))[c]; }
+        for (int i = 0; i < 3; ++i) Xt[i] = F(XT + i)[c];
+        double dphi[3], dtrK[3], dgt[3][3][3], dAt[3][3][3], dXt[3][3];
+        for (int l = 0; l < 3; ++l) {
+          dphi[l] = d1(F(PHI), c, st[l], h[l]);
+          dtrK[l] = d1(F(TRK), c, st[l], h[l]);
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+              dgt[l][i][j] = d1(F(GT + sym(i, j)), c, st[l], h[l]);
+              dAt[l][i][j] = d1(F(AT + sym(i, j)), c, st[l], h[l]);
+            }
+          for (int kx = 0; kx < 3; ++kx) dXt[l][kx] = d1(F(XT + kx), c, st[l], h[l]);
+        }
+        auto dd = [&](int v, int l, int m) {
+          if (l == m) return d2(F(v), c, st[l], h[l]);
+          return d11(F(v), c, st[l], h[l], st[m], h[m]);
+        };
+        const double det = gt[0][0] * (gt[1][1] * gt[2][2] - gt[1][2] * gt[2][1]) -
+                           gt[0][1] * (gt[1][0] * gt[2][2] - gt[1][2] * gt[2][0]) +
+                           gt[0][2] * (gt[1][0] * gt[2][1] - gt[1][1] * gt[2][0]);
+        double gu[3][3];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            const int r0 = (j + 1) % 3, r1 = (j + 2) % 3, c0 = (i + 1) % 3, c1 = (i + 2) % 3;
+            gu[i][j] = (gt[r0][c0] * gt[r1][c1] - gt[r0][c1] * gt[r1][c0]) / det;
+          }
+        double Gl[3][3][3], Gu[3][3][3], Xtn[3];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j)
+            for (int kx = 0; kx < 3; ++kx)
+              Gl[i][j][kx] = 0.5 * (dgt[j][i][kx] + dgt[kx][i][j] - dgt[i][j][kx]);
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j)
+            for (int kx = 0; kx < 3; ++kx) {
+              double s = 0.0;
+              for (int l = 0; l < 3; ++l) s += gu[i][l] * Gl[l][j][kx];
+              Gu[i][j][kx] = s;
+            }
+        for (int i = 0; i < 3; ++i) {
+          double s = 0.0;
+          for (int j = 0; j < 3; ++j)
+            for (int kx = 0; kx < 3; ++kx) s += gu[j][kx] * Gu[i][j][kx];
+          Xtn[i] = s;
+        }
+        // Ricci scalar: gt^ij (R~_ij + R^phi_ij), as in the RHS
+        double Rsum = 0.0;
+        double trDDphi = 0.0, dphi2 = 0.0, DDphi[3][3];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            double s = dd(PHI, i, j);
+            for (int kx = 0; kx < 3; ++kx) s -= Gu[kx][i][j] * dphi[kx];
+            DDphi[i][j] = s;
+          }
+        for (int l = 0; l < 3; ++l)
+          for (int m = 0; m < 3; ++m) {
+            trDDphi += gu[l][m] * DDphi[l][m];
+            dphi2 += gu[l][m] * dphi[l] * dphi[m];
+          }
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int l = 0; l < 3; ++l)
+              for (int m = 0; m < 3; ++m) s += gu[l][m] * dd(GT + sym(i, j), l, m);
+            double r = -0.5 * s;
+            for (int kx = 0; kx < 3; ++kx)
+              r += 0.5 * (gt[kx][i] * dXt[j][kx] + gt[kx][j] * dXt[i][kx]);
+            for (int kx = 0; kx < 3; ++kx) r += 0.5 * Xtn[kx] * (Gl[i][j][kx] + Gl[j][i][kx]);
+            for (int l = 0; l < 3; ++l)
+              for (int m = 0; m < 3; ++m)
+                for (int kx = 0; kx < 3; ++kx)
+                  r += gu[l][m] * (Gu[kx][l][i] * Gl[j][kx][m] + Gu[kx][l][j] * Gl[i][kx][m] +
+                                   Gu[kx][i][m] * Gl[kx][l][j]);
+            const double Rphi = -2.0 * DDphi[i][j] - 2.0 * gt[i][j] * trDDphi + 4.0 * dphi[i] * dphi[j] -
+                                4.0 * gt[i][j] * dphi2;
+            Rsum += gu[i][j] * (r + Rphi);
+          }
+        const double Rscal = std::exp(-4.0 * phi) * Rsum;
+        double Atu[3][3];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int kx = 0; kx < 3; ++kx)
+              for (int l = 0; l < 3; ++l) s += gu[i][kx] * gu[j][l] * At[kx][l];
+            Atu[i][j] = s;
+          }
+        double AA = 0.0;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) AA += At[i][j] * Atu[i][j];
+        out[0 * ni + o] = Rscal + (2.0 / 3.0) * trK * trK - AA;
+        // d_l gu^{ab} = -gu^{ai} gu^{bj} d_l gt_ij
+        double dgu[3][3][3];
+        for (int l = 0; l < 3; ++l)
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+              double s = 0.0;
+              for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) s -= gu[a][i] * gu[b][j] * dgt[l][i][j];
+              dgu[l][a][b] = s;
+            }
+        for (int i = 0; i < 3; ++i) {
+          // d_j At^ij = d_j (gu^ik gu^jl At_kl)
+          double div = 0.0;
+          for (int j = 0; j < 3; ++j)
+            for (int kx = 0; kx < 3; ++kx)
+              for (int l = 0; l < 3; ++l)
+                div += dgu[j][i][kx] * gu[j][l] * At[kx][l] + gu[i][kx] * dgu[j][j][l] * At[kx][l] +
+                       gu[i][kx] * gu[j][l] * dAt[j][kx][l];
+          double m = div;
+          for (int j = 0; j < 3; ++j)
+            for (int kx = 0; kx < 3; ++kx) m += Gu[i][j][kx] * Atu[j][kx];
+          for (int j = 0; j < 3; ++j) m += 6.0 * Atu[i][j] * dphi[j] - (2.0 / 3.0) * gu[i][j] * dtrK[j];
+          out[(1 + i) * ni + o] = m;
+          out[(4 + i) * ni + o] = Xt[i] - Xtn[i];
+        }
+      }
+}
+
 int n_gf_of(int system) { return system == 1 ? 5 : (system == 2 ? 25 : -1); }
 
 const double kDefaultBssnParams[10] = {2.0, 1.0, 1.0, 0.0, 1.0, 0.75, 0.0, 1.0, 1.0, 1.0};
@@ -580,6 +717,16 @@ int chemora_oracle_norms(int system, const double* y, const int64_t* ext, int g,
     for (int64_t z = 0; z < nz; ++z) e += en[z];
     out[3 * nf] = vol * e;
   }
+  return 0;
+}
+
+// BSSN constraint fields at interior points, ghosts of y used as they are.
+// out: 7 interior arrays [H, M1, M2, M3, G1, G2, G3] (see bssn_constraints above).
+int chemora_oracle_constraints(const double* y, const int64_t* ext, int g, const double* spacing,
+                               double* out) {
+  if (g < 3) return 2;
+  Grid G(ext, g, spacing);
+  bssn_constraints(y, out, G);
   return 0;
 }
 
