@@ -192,6 +192,23 @@ int chemora_set_monitor(chemora_grid_t grid, int enable);
 int chemora_read_monitor(chemora_grid_t grid, double* out, int32_t max, int32_t* count,
                          void* stream);
 
+/* BSSN constraint monitors ("constraint equations"; SURVEY.md §8(f)
+ * NEXT-3; reading R16), from the current state y with the RHS's 4th-order
+ * stencils (ghosts of y used as they are -- consistent after every call that returns y):
+ *   H   = e^{-4 phi} gt^ij (R~_ij + R^phi_ij) + 2/3 K^2 - At_ij At^ij
+ *   M^i = d_j At^ij + Gt^i_jk At^jk + 6 At^ij d_j phi - 2/3 gt^ij d_j K
+ *   G^i = Xt^i - gt^jk Gt^i_jk
+ * dev_fields (device, nullable): 7 x local interior, [H, M1, M2, M3, G1, G2, G3][z][y][x],
+ * caller-owned.  host_out (nullable, 14 doubles): per constraint q, the local partials
+ * host_out[2q] = sum c_q^2 and host_out[2q+1] = max |c_q| in a fixed (deterministic) order;
+ * with nranks == 1, chemora_constraint_norms turns them into L2 = sqrt(h^3 sum) and Linf.
+ * BSSN only (CHEMORA_E_UNSUPPORTED otherwise).  Synchronises the stream when host_out is
+ * given. */
+int chemora_constraints(chemora_grid_t grid, double* dev_fields, double* host_out, void* stream);
+
+/* nranks == 1: out[2q] = L2 = sqrt(h^3 sum c_q^2), out[2q+1] = Linf of the 7 constraints. */
+int chemora_constraint_norms(chemora_grid_t grid, double* host_out, void* stream);
+
 /* Model-driven tiling choice ("autotuning is model driven"): a
  * footprint/occupancy model prunes the stage-kernel tilings to <= 4 candidates, each is
  * timed on `trials` stage-1 launches (dt = 0: the state is not modified, the scratch set B

@@ -66,6 +66,8 @@ _SIGS = {
     "chemora_norms_combine": ([_descp, _dp, ctypes.c_int32, _dp], ctypes.c_int),
     "chemora_norms_len": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
     "chemora_norms": ([_vp, _dp, _vp], ctypes.c_int),
+    "chemora_constraints": ([_vp, _vp, _dp, _vp], ctypes.c_int),
+    "chemora_constraint_norms": ([_vp, _dp, _vp], ctypes.c_int),
     "chemora_grid_connect_local": ([ctypes.POINTER(_vp), ctypes.c_int32], ctypes.c_int),
     "chemora_peer_record_size": ([ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "chemora_grid_export_peer": ([_vp, _vp], ctypes.c_int),
@@ -213,6 +215,21 @@ def chemora_norms_combine(desc, partials: np.ndarray, nranks: int) -> np.ndarray
 def chemora_norms(h, system, stream=None) -> np.ndarray:
     out = np.zeros(chemora_norms_len(system))
     _check(_lib.chemora_norms(h, _dptr(out), stream), "chemora_norms")
+    return out
+
+
+def chemora_constraints(h, dev_fields_ptr: int | None = None, partials: bool = True, stream=None):
+    """BSSN constraint fields into a device buffer (optional) and/or the 14 local partials
+    [sum c_q^2, max |c_q|] x (H, M1..3, G1..3)."""
+    out = np.zeros(14) if partials else None
+    _check(_lib.chemora_constraints(h, _vp(dev_fields_ptr) if dev_fields_ptr else None, _dptr(out), stream),
+           "chemora_constraints")
+    return out
+
+
+def chemora_constraint_norms(h, stream=None) -> np.ndarray:
+    out = np.zeros(14)
+    _check(_lib.chemora_constraint_norms(h, _dptr(out), stream), "chemora_constraint_norms")
     return out
 
 

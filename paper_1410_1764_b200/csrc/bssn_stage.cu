@@ -433,6 +433,206 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
   }
 }
 
+// ------------------------------------------------------------------ constraint monitors
+// Vacuum BSSN constraints (R16) with
+// the RHS's stencils and Ricci tensor:
+//   c[0] = H   = e^{-4 phi} gt^ij (R~_ij + R^phi_ij) + 2/3 K^2 - At_ij At^ij
+//   c[1+i] = M^i = d_j At^ij + Gt^i_jk At^jk + 6 At^ij d_j phi - 2/3 gt^ij d_j K
+//   c[4+i] = G^i = Xt^i - gt^jk Gt^i_jk
+// d_j At^ij by the product rule with d_j gt^ab = -gt^ac (d_j gt_cd) gt^db.
+__device__ __forceinline__ void bssn_constraint_point(const StencilP& D, const BssnK& K, double* c) {
+  double gt[6], At[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) { gt[s] = D.v(V_GT + s); At[s] = D.v(V_AT + s); }
+  const double phi = D.v(V_PHI), trK = D.v(V_TRK);
+  const double c00 = gt[3] * gt[5] - gt[4] * gt[4];
+  const double c01 = gt[2] * gt[4] - gt[1] * gt[5];
+  const double c02 = gt[1] * gt[4] - gt[2] * gt[3];
+  const double idet = 1.0 / (gt[0] * c00 + gt[1] * c01 + gt[2] * c02);
+  double gu[6];
+  gu[0] = c00 * idet;
+  gu[1] = c01 * idet;
+  gu[2] = c02 * idet;
+  gu[3] = (gt[0] * gt[5] - gt[2] * gt[2]) * idet;
+  gu[4] = (gt[1] * gt[2] - gt[0] * gt[4]) * idet;
+  gu[5] = (gt[0] * gt[3] - gt[1] * gt[1]) * idet;
+  double dg[3][6], Gl[3][6], Gu[3][6], Xtn[3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int s = 0; s < 6; ++s) dg[l][s] = D.d1(K, V_GT + s, l);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int j = sI(s), k = sJ(s);
+      Gl[i][s] = 0.5 * (dg[j][sy(i, k)] + dg[k][sy(i, j)] - dg[i][s]);
+    }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      Gu[i][s] = gu[sy(i, 0)] * Gl[0][s] + gu[sy(i, 1)] * Gl[1][s] + gu[sy(i, 2)] * Gl[2][s];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) a = fma(mult(s) * gu[s], Gu[i][s], a);
+    Xtn[i] = a;
+  }
+  double dphi[3], dtrK[3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) { dphi[l] = D.d1(K, V_PHI, l); dtrK[l] = D.d1(K, V_TRK, l); }
+  double Am[3][3], Au[6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      Am[i][j] = gu[sy(i, 0)] * At[sy(0, j)] + gu[sy(i, 1)] * At[sy(1, j)] + gu[sy(i, 2)] * At[sy(2, j)];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int i = sI(s), j = sJ(s);
+    Au[s] = Am[i][0] * gu[sy(0, j)] + Am[i][1] * gu[sy(1, j)] + Am[i][2] * gu[sy(2, j)];
+  }
+  // ---- Hamiltonian: Ricci scalar as in bssn_point's curvature group
+  {
+    double Rt[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) Rt[s] = 0.0;
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const int l = sI(p), m = sJ(p);
+      const double w = -0.5 * mult(p) * gu[p];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) Rt[s] = fma(w, D.dd(K, V_GT + s, l, m, gt[s]), Rt[s]);
+    }
+    double Rsum = 0.0, DDphi[6], trDDphi = 0.0, dphi2 = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int i = sI(s), j = sJ(s);
+      DDphi[s] = D.dd(K, V_PHI, i, j, phi) - (Gu[0][s] * dphi[0] + Gu[1][s] * dphi[1] + Gu[2][s] * dphi[2]);
+      trDDphi = fma(mult(s) * gu[s], DDphi[s], trDDphi);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      dphi2 = fma(gu[sy(k, 0)] * dphi[0] + gu[sy(k, 1)] * dphi[1] + gu[sy(k, 2)] * dphi[2], dphi[k], dphi2);
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int i = sI(s), j = sJ(s);
+      double r = Rt[s];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        r = fma(0.5 * gt[sy(k, i)], D.d1(K, V_XT + k, j), r);
+        r = fma(0.5 * gt[sy(k, j)], D.d1(K, V_XT + k, i), r);
+        r = fma(0.5 * Xtn[k], Gl[i][sy(j, k)] + Gl[j][sy(i, k)], r);
+      }
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            t = fma(Gu[k][sy(l, i)], Gl[j][sy(k, m)], t);
+            t = fma(Gu[k][sy(l, j)], Gl[i][sy(k, m)], t);
+            t = fma(Gu[k][sy(i, m)], Gl[k][sy(l, j)], t);
+          }
+          r = fma(gu[sy(l, m)], t, r);
+        }
+      const double Rphi = -2.0 * DDphi[s] - 2.0 * gt[s] * trDDphi + 4.0 * dphi[i] * dphi[j] - 4.0 * gt[s] * dphi2;
+      Rsum = fma(mult(s) * gu[s], r + Rphi, Rsum);
+    }
+    double AA = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) AA = fma(mult(s) * At[s], Au[s], AA);
+    c[0] = exp(-4.0 * phi) * Rsum + (2.0 / 3.0) * trK * trK - AA;
+  }
+  // ---- momentum and Gamma constraints
+  double W[3] = {0.0, 0.0, 0.0}, U[3] = {0.0, 0.0, 0.0}, V[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    double dAt[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) dAt[s] = D.d1(K, V_AT + s, j);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        W[k] = fma(gu[sy(j, l)], dAt[sy(k, l)], W[k]);      // gt^jl d_j At_kl
+        U[k] = fma(dg[j][sy(k, l)], Au[sy(l, j)], U[k]);    // d_j gt_kl At^lj
+        V[l] = fma(gu[sy(j, k)], dg[j][sy(k, l)], V[l]);    // gt^jk d_j gt_kl
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double m = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      m = fma(gu[sy(i, k)], W[k] - U[k], m);
+      m = fma(-Au[sy(i, k)], V[k], m);
+      m = fma(6.0 * Au[sy(i, k)], dphi[k], m);
+      m = fma(-(2.0 / 3.0) * gu[sy(i, k)], dtrK[k], m);
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) m = fma(mult(q) * Gu[i][q], Au[q], m);
+    c[1 + i] = m;
+    c[4 + i] = D.v(V_XT + i) - Xtn[i];
+  }
+}
+
+// One thread per point over a fixed grid of kNormBlocks CTAs (grid-stride over the
+// interior in a fixed order, so the partials -- and the norms -- are deterministic).
+// fields (nullable): [7][z][y][x] interior; part: per CTA [sum c_q^2, max |c_q|] x 7.
+constexpr int kConThreads = 128;
+__global__ void __launch_bounds__(kConThreads) bssn_constraints_kernel(Layout L, const double* in, BssnK K,
+                                                                       double* fields, double* part) {
+  __shared__ double sh[kConThreads / 32][14];
+  double acc[14];
+#pragma unroll
+  for (int q = 0; q < 14; ++q) acc[q] = 0.0;
+  const int64_t ni = L.nx * L.ny * L.nz;
+  for (int64_t p = (int64_t)blockIdx.x * kConThreads + threadIdx.x; p < ni; p += (int64_t)gridDim.x * kConThreads) {
+    const int i = (int)(p % L.nx);
+    const int j = (int)((p / L.nx) % L.ny);
+    const int k = (int)(p / (L.nx * L.ny));
+    StencilP P{in, L.gfs, L.idx(i, j, k), {{1, L.px, L.plane}}};
+    double c[7];
+    bssn_constraint_point(P, K, c);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      if (fields) fields[q * ni + p] = c[q];
+      acc[2 * q] = fma(c[q], c[q], acc[2 * q]);
+      acc[2 * q + 1] = fmax(acc[2 * q + 1], fabs(c[q]));
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 14; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (q & 1) ? fmax(v, u) : v + u;
+    }
+    if (lane == 0) sh[w][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 14) {
+    const int q = threadIdx.x;
+    double v = sh[0][q];
+    for (int ww = 1; ww < kConThreads / 32; ++ww) v = (q & 1) ? fmax(v, sh[ww][q]) : v + sh[ww][q];
+    part[(int64_t)blockIdx.x * 14 + q] = v;
+  }
+}
+
+__global__ void bssn_constraints_combine(const double* part, int nblocks, double* out) {
+  const int q = threadIdx.x;
+  if (q >= 14) return;
+  double v = 0.0;
+  for (int b = 0; b < nblocks; ++b) v = (q & 1) ? fmax(v, part[(int64_t)b * 14 + q]) : v + part[(int64_t)b * 14 + q];
+  out[q] = v;
+}
+
 BssnK make_k(const StageLaunch& a, const double* prm) {
   BssnK K;
   for (int d = 0; d < 3; ++d) {
@@ -658,6 +858,13 @@ cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st) {
 }
 cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st) {
   return dispatch(a, 0, dst, st, a.hparams);
+}
+cudaError_t bssn_constraints(const StageLaunch& a, double* fields, double* scratch, double* out_dev,
+                             cudaStream_t st) {
+  const BssnK K = make_k(a, a.hparams);
+  bssn_constraints_kernel<<<kNormBlocks, kConThreads, 0, st>>>(a.L, a.s.y, K, fields, scratch);
+  bssn_constraints_combine<<<1, 32, 0, st>>>(scratch, kNormBlocks, out_dev);
+  return cudaGetLastError();
 }
 
 }  // namespace chemora

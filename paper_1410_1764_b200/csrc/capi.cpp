@@ -812,6 +812,31 @@ int chemora_norms(chemora_grid_t g, double* out, void* stream) {
   return rc ? rc : rc2;
 }
 
+int chemora_constraints(chemora_grid_t g, double* fields, double* out, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (g->desc.system != CHEMORA_SYS_BSSN) return fail(CHEMORA_E_UNSUPPORTED, "constraints: BSSN only");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  StageLaunch a = stage_args(g, 0.0);
+  CUDA_TRY(bssn_constraints(a, fields, g->norm_scratch, g->norm_out, st));
+  if (!out) return CHEMORA_OK;
+  CUDA_TRY(cudaMemcpyAsync(out, g->norm_out, sizeof(double) * 14, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return read_nan_flag(g, st);
+}
+
+int chemora_constraint_norms(chemora_grid_t g, double* out, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!out) return fail(CHEMORA_E_INVALID, "out is NULL");
+  if (g->desc.nranks > 1)
+    return fail(CHEMORA_E_UNSUPPORTED, "nranks > 1: gather chemora_constraints partials");
+  int rc = chemora_constraints(g, nullptr, out, stream);
+  if (rc && rc != CHEMORA_E_NONFINITE) return rc;
+  const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
+  for (int q = 0; q < 7; ++q) out[2 * q] = std::sqrt(vol * out[2 * q]);
+  return rc;
+}
+
 int chemora_grid_connect_local(chemora_grid_t* grids, int32_t n) {
   if (!grids || n < 1) return fail(CHEMORA_E_INVALID, "bad grid list");
   for (int r = 0; r < n; ++r) {

@@ -52,6 +52,11 @@ cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st);
 // BSSN (App. A) ------------------------------------------------------------------------
 cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st);
 cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
+// BSSN constraints H, M^i, G^i of a.s.y (R16): optional interior fields
+// [7][z][y][x] (nullable) and, on the device, out_dev[2q] = sum c_q^2, out_dev[2q+1] =
+// max |c_q| (scratch: kNormBlocks x 14 doubles).
+cudaError_t bssn_constraints(const StageLaunch& a, double* fields, double* scratch, double* out_dev,
+                             cudaStream_t st);
 
 // Ghost fill of one set (all GFs): x and y locally, then z images stored to face bases.
 cudaError_t ghost_fill(const Layout& L, double* set, FaceDst z, cudaStream_t st);

@@ -36,3 +36,17 @@ def gather_partials(partials: np.ndarray, world: int, group=None) -> np.ndarray:
     out = [None] * world
     dist.all_gather_object(out, np.asarray(partials, dtype=np.float64).tolist(), group=group)
     return np.array(out, dtype=np.float64)
+
+
+def combine_constraint_partials(gathered: np.ndarray, vol: float) -> np.ndarray:
+    """Rank-major [world][14] partials [sum c_q^2, max |c_q|] x 7 of chemora_constraints ->
+    [L2_q, Linf_q] x 7 (sums in rank order, so the result is deterministic)."""
+    g = np.asarray(gathered, dtype=np.float64).reshape(-1, 14)
+    out = np.zeros(14)
+    for q in range(7):
+        s = 0.0
+        for r in range(g.shape[0]):
+            s += g[r, 2 * q]
+        out[2 * q] = np.sqrt(vol * s)
+        out[2 * q + 1] = g[:, 2 * q + 1].max()
+    return out

@@ -76,6 +76,24 @@ class Grid:
         gathered = D.gather_partials(part, self.nranks, group)
         return C.chemora_norms_combine(self.desc, gathered, self.nranks)
 
+    def constraints(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """BSSN constraint fields [H, M1, M2, M3, G1, G2, G3][z][y][x] of the current state."""
+        if out is None:
+            n = self.interior_shape()
+            out = torch.empty((7,) + tuple(n[1:]), dtype=torch.float64, device=self.device)
+        assert out.is_contiguous() and out.dtype == torch.float64
+        C.chemora_constraints(self.handle, out.data_ptr(), False, self.stream)
+        return out
+
+    def constraint_norms(self, group=None) -> np.ndarray:
+        """[L2, Linf] of H, M1..3, G1..3 (14 doubles), over all ranks."""
+        if self.nranks == 1:
+            return C.chemora_constraint_norms(self.handle, self.stream)
+        part = C.chemora_constraints(self.handle, None, True, self.stream)
+        gathered = D.gather_partials(part, self.nranks, group)
+        h = self.desc.spacing
+        return D.combine_constraint_partials(gathered, h[0] * h[1] * h[2])
+
     def connect_ipc(self, group=None):
         """Exchange peer records over torch.distributed and open the ring neighbours."""
         rec = C.chemora_grid_export_peer(self.handle)

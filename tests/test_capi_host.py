@@ -116,3 +116,17 @@ def test_norms_combine_host_logic():
     assert out[1] == 7.0
     assert out[2] == pytest.approx(0.125 * 3.0)
     assert out[15] == pytest.approx(0.125 * 3.0)
+
+
+def test_combine_constraint_partials():
+    """Rank-major constraint partials -> L2 = sqrt(h^3 sum), Linf = max over ranks."""
+    import numpy as np
+    from paper_1410_1764_b200 import dist as D
+    parts = np.zeros((2, 14))
+    parts[0, 0::2] = np.arange(7) + 1.0
+    parts[1, 0::2] = 2.0 * (np.arange(7) + 1.0)
+    parts[0, 1::2] = 0.5
+    parts[1, 1::2] = np.linspace(0.1, 0.9, 7)
+    out = D.combine_constraint_partials(parts.ravel(), 0.125)
+    assert np.allclose(out[0::2], np.sqrt(0.125 * 3.0 * (np.arange(7) + 1.0)), rtol=1e-15)
+    assert np.array_equal(out[1::2], np.maximum(0.5, np.linspace(0.1, 0.9, 7)))
