@@ -65,6 +65,21 @@ __device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity)
   }
 }
 
+// Wait with a suspend-time hint: the thread is suspended until the phase completes (or the
+// hint, in ns, expires) instead of re-polling -- for a producer thread that runs ahead of
+// its consumers, so its polling does not take issue slots from the consumer warps.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 // 4-D tiled TMA load (coords innermost first) completing on an mbarrier.
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {

@@ -58,13 +58,17 @@ constexpr int PY_R = r128(IR_X * IR_Y * 8), PY_1 = r128(I1_X * I1_Y * 8), PY_2 =
               PY_3 = r128(I3_X * I3_Y * 8);
 constexpr int IZ_B = r128(IR_X * IR_Y * 8) + r128(I3_X * I3_Y * 8);  // intermediate z ring slot
 constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermediate p ring slot
-constexpr int RI_Z = 5, RI_P = 3;
+// The second stage runs 3 planes behind the first (k = p - 3), so within one iteration the
+// two stages touch disjoint intermediate slots and a single CTA barrier per plane suffices:
+// the z ring holds planes p-5 .. p (6 slots), the v1/v2 ring planes p-3 .. p (4 slots).
+constexpr int LAG = 3;
+constexpr int RI_Z = 6, RI_P = 4;
 
 template <bool B> struct Geo {
-  // input ring depths: kernel A has the shared memory for 5 (Z) / 5 (P) planes of
-  // prefetch beyond the resident window; kernel B (more operands) for 2 / 1
-  static constexpr int RZ = B ? 7 : 10;
-  static constexpr int RP = B ? 4 : 8;
+  // input ring depths: resident windows are Z: planes p-3 .. p+2 (6), P: p-3 .. p (A) or p
+  // (B), Q: k (B); the rest is prefetch
+  static constexpr int RZ = B ? 8 : 10;
+  static constexpr int RP = B ? 3 : 8;
   static constexpr int RQ = B ? 3 : 0;
   static constexpr int PSLOT = P1_B + P2_B + (B ? PY_R + PY_1 + PY_2 + PY_3 : 0);
   static constexpr uint32_t PBYTES =
@@ -78,6 +82,7 @@ template <bool B> struct Geo {
   static constexpr int OFF_BAR = OFF_IP + RI_P * IP_B;
   static constexpr int NBAR = 2 * RZ + 2 * RP + 2 * RQ;
   static constexpr int SMEM = OFF_BAR + NBAR * 8;
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 struct FMaps {
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int xo = kXOff + i0, yo = g + j0;
       auto loadZ = [&](int plane) {
         const uint32_t s = nz % G::RZ, n = nz / G::RZ;
-        if (n > 0) mbar_wait(zempty + s, (n - 1) & 1);
+        if (n > 0) mbar_wait_suspend(zempty + s, (n - 1) & 1);
         unsigned char* d = smem + s * ZSLOT;
         mbar_arrive_expect_tx(zfull + s, ZBYTES);
         tma_load_4d(d, &M.rho, zfull + s, xo - H, yo - H, g + plane, GRHO);
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(NT, 1)
       };
       auto loadP = [&](int plane) {
         const uint32_t s = np % G::RP, n = np / G::RP;
-        if (n > 0) mbar_wait(pempty + s, (n - 1) & 1);
+        if (n > 0) mbar_wait_suspend(pempty + s, (n - 1) & 1);
         unsigned char* d = smem + G::OFF_P + s * G::PSLOT;
         uint64_t* bar = pfull + s;
         mbar_arrive_expect_tx(bar, G::PBYTES);
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(NT, 1)
       };
       auto loadQ = [&](int plane) {
         const uint32_t s = nq % G::RQ, n = nq / G::RQ;
-        if (n > 0) mbar_wait(qempty + s, (n - 1) & 1);
+        if (n > 0) mbar_wait_suspend(qempty + s, (n - 1) & 1);
         unsigned char* d = smem + G::OFF_Q + s * G::QSLOT;
         mbar_arrive_expect_tx(qfull + s, G::QBYTES);
         tma_load_4d(d, &M.q5, qfull + s, xo, yo, g + plane, GU);
@@ -170,8 +175,10 @@ __global__ void __launch_bounds__(NT, 1)
         const int p = kb - 2 + j;
         loadZ(p + 2);
         loadP(p);
-        if (B && p - 2 >= kb) loadQ(p - 2);
+        if (B && p - LAG >= kb) loadQ(p - LAG);
       }
+      if (B)
+        for (int k = kb + nk + 2 - LAG; k < kb + nk; ++k) loadQ(k);
     }
     return;
   }
@@ -244,85 +251,89 @@ __global__ void __launch_bounds__(NT, 1)
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
     int64_t cglob = L.idx(i, j, kb);  // global offset of this thread's point at plane k
-    // ring slots: input planes p-2..p+2, P planes p and p-2, intermediate planes
-    int zsl[5];
+    // ring slots: input planes p-3 .. p+2 (zsl[0] is only meaningful once jj >= 1)
+    int zsl[6];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) zsl[q] = (int)((z0 + q) % G::RZ);
-    int psl = (int)(p0 % G::RP), psl2 = 0;   // P slot of plane p, of plane p-2
-    int zph = (int)(((z0 + 4) / G::RZ) & 1);    // phase of the input slot zsl[4]
+    for (int q = 0; q < 6; ++q) zsl[q] = (int)((z0 + G::RZ + q - 1) % G::RZ);
+    int zph = (int)(((z0 + 4) / G::RZ) & 1);    // phase of the input slot zsl[5]
+    int psl = (int)(p0 % G::RP);                // P slot of plane p
     int pph = (int)((p0 / G::RP) & 1);
-    int izs[5] = {0, 0, 0, 0, 0};           // intermediate z slots of planes p-4..p
-    int ips[3] = {0, 0, 0};                 // intermediate p slots of planes p-2..p
+    int pslk = psl;                             // P slot of plane k = p - 3 (A, jj >= 3)
+    int izs[6] = {0, 0, 0, 0, 0, 0};            // intermediate z slots of planes p-5 .. p
+    int ips[4] = {0, 0, 0, 0};                  // intermediate p slots of planes p-3 .. p
 #pragma unroll 1
-    for (int jj = 0; jj < nk + 4; ++jj) {
+    for (int jj = 0; jj < nk + 4 + 1; ++jj) {
       const int p = kb - 2 + jj;
-      // intermediate slot of plane p (jj mod 5 / mod 3), kept incrementally
+      const bool first = jj < nk + 4;           // intermediate plane p is needed
+      const int k = p - LAG;
+      const bool second = k >= kb;              // output plane k
 #pragma unroll
-      for (int q = 0; q < 4; ++q) izs[q] = izs[q + 1];
-      izs[4] = jj % RI_Z;
-      ips[0] = ips[1];
-      ips[1] = ips[2];
-      ips[2] = jj % RI_P;
-      mbar_wait(zfull + zsl[4], zph);
-      mbar_wait(pfull + psl, pph);
-      const double* zR[5];
-      const double* z3[5];
+      for (int q = 0; q < 5; ++q) izs[q] = izs[q + 1];
+      izs[5] = jj % RI_Z;
 #pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        zR[q] = sm + zsl[q] * ZSD;
-        z3[q] = zR[q] + ZR_D;
+      for (int q = 0; q < 3; ++q) ips[q] = ips[q + 1];
+      ips[3] = jj % RI_P;
+      cbar();  // the previous plane's intermediate values are complete and its reads done
+      if (first) {
+        mbar_wait(zfull + zsl[5], zph);
+        mbar_wait(pfull + psl, pph);
+        const double* zR[5];
+        const double* z3[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          zR[q] = sm + zsl[q + 1] * ZSD;
+          z3[q] = zR[q] + ZR_D;
+        }
+        const double* s1 = sm + OFF_PD + psl * PSD;
+        const double* s2 = s1 + P1D;
+        const double* sy = s2 + P2D;  // B only
+        double* IR = sm + OFF_IZD + izs[5] * IZD;
+        double* I3 = IR + IR_D;
+        double* I1 = sm + OFF_IPD + ips[3] * IPD;
+        double* I2 = I1 + I1_D;
+        // ---- intermediate state at plane p: Y2 = y + dt/2 k1(y) (A) or Y4 = y + dt k3(C) (B)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!rR_ok[u]) continue;
+          const double dv1 = d1s_(s1, rR_c1[u], 1) * K.ih[0];
+          const double dv2 = d1s_(s2, rR_c2[u], B2_X) * K.ih[1];
+          double dv3 = 0.0;
+#pragma unroll
+          for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][rR_c3[u]] - z3[2 - q][rR_c3[u]], dv3);
+          dv3 = dv3 * K.ih[2];
+          const double kr = dv1 + dv2 + dv3;
+          const int e = tid + u * NTC;
+          const double base = B ? sy[e] : zR[2][rR_b[u]];
+          IR[e] = fma(cdt, kr, base);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!r1_ok[u]) continue;
+          const int e = tid + u * NTC;
+          const double kr = d1s_(zR[2], r1_cr[u], 1) * K.ih[0];
+          const double base = B ? sy[PYR + e] : s1[r1_b[u]];
+          I1[e] = fma(cdt, kr, base);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!r2_ok[u]) continue;
+          const int e = tid + u * NTC;
+          const double kr = d1s_(zR[2], r2_cr[u], BR_X) * K.ih[1];
+          const double base = B ? sy[PYR + PY1 + e] : s2[r2_b[u]];
+          I2[e] = fma(cdt, kr, base);
+        }
+        {
+          double dzr = 0.0;
+#pragma unroll
+          for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[2 + q][r3_cr] - zR[2 - q][r3_cr], dzr);
+          const double kr = dzr * K.ih[2];
+          const double base = B ? sy[PYR + PY1 + PY2 + tid] : z3[2][r3_b];
+          I3[tid] = fma(cdt, kr, base);
+        }
       }
-      const double* s1 = sm + OFF_PD + psl * PSD;
-      const double* s2 = s1 + P1D;
-      const double* sy = s2 + P2D;  // B only
-      double* IR = sm + OFF_IZD + izs[4] * IZD;
-      double* I3 = IR + IR_D;
-      double* I1 = sm + OFF_IPD + ips[2] * IPD;
-      double* I2 = I1 + I1_D;
-      cbar();  // everyone is done with the intermediate slots being overwritten
-      // ---- intermediate state at plane p: Y2 = y + dt/2 k1(y) (A) or Y4 = y + dt k3(C) (B)
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!rR_ok[u]) continue;
-        const double dv1 = d1s_(s1, rR_c1[u], 1) * K.ih[0];
-        const double dv2 = d1s_(s2, rR_c2[u], B2_X) * K.ih[1];
-        double dv3 = 0.0;
-#pragma unroll
-        for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][rR_c3[u]] - z3[2 - q][rR_c3[u]], dv3);
-        dv3 = dv3 * K.ih[2];
-        const double k = dv1 + dv2 + dv3;
-        const int e = tid + u * NTC;
-        const double base = B ? sy[e] : zR[2][rR_b[u]];
-        IR[e] = fma(cdt, k, base);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!r1_ok[u]) continue;
-        const int e = tid + u * NTC;
-        const double k = d1s_(zR[2], r1_cr[u], 1) * K.ih[0];
-        const double base = B ? sy[PYR + e] : s1[r1_b[u]];
-        I1[e] = fma(cdt, k, base);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!r2_ok[u]) continue;
-        const int e = tid + u * NTC;
-        const double k = d1s_(zR[2], r2_cr[u], BR_X) * K.ih[1];
-        const double base = B ? sy[PYR + PY1 + e] : s2[r2_b[u]];
-        I2[e] = fma(cdt, k, base);
-      }
-      {
-        double dzr = 0.0;
-#pragma unroll
-        for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[2 + q][r3_cr] - zR[2 - q][r3_cr], dzr);
-        const double k = dzr * K.ih[2];
-        const double base = B ? sy[PYR + PY1 + PY2 + tid] : z3[2][r3_b];
-        I3[tid] = fma(cdt, k, base);
-      }
-      cbar();  // the intermediate plane p is complete
-      // ---- second stage at plane k = p - 2
-      const int k = p - 2;
-      if (k >= kb) {
+      // ---- second stage at plane k = p - 3 (its intermediate planes k-2 .. k+2 were
+      // completed in earlier iterations)
+      if (second) {
         const double* iR[5];
         const double* i3[5];
 #pragma unroll
@@ -332,6 +343,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         const double* i1 = sm + OFF_IPD + ips[0] * IPD;
         const double* i2 = i1 + I1_D;
+        const double* zk = sm + zsl[0] * ZSD;   // input plane k
         double S[5], kk[5];
         S[GRHO] = iR[2][s_cr];
         S[GV1] = i1[s_c1];
@@ -355,18 +367,18 @@ __global__ void __launch_bounds__(NT, 1)
         kk[GV3] = dzr;
         double Y[5] = {0, 0, 0, 0, 0}, Qv[5] = {0, 0, 0, 0, 0}, yu = 0.0, qu = 0.0;
         if (!B) {
-          // y at plane k: input plane k = p - 2 (zR[0]), P plane k (slot psl2)
-          const double* k1 = sm + OFF_PD + psl2 * PSD;
+          // y at plane k: input plane k (zk), P plane k (slot pslk)
+          const double* k1 = sm + OFF_PD + pslk * PSD;
           const double* k2 = k1 + P1D;
-          Y[GRHO] = zR[0][y_r];
+          Y[GRHO] = zk[y_r];
           Y[GV1] = k1[y_1];
           Y[GV2] = k2[y_2];
-          Y[GV3] = z3[0][y_3];
+          Y[GV3] = zk[ZR_D + y_3];
         } else {
           mbar_wait(qfull + nq % G::RQ, (nq / G::RQ) & 1);
           const double* qs = sm + OFF_QD + (nq % G::RQ) * (G::QSLOT / 8);
           // u carry of stage 3 (folded): Q.u += dt/3 C.rho, with C.rho at plane k from the ring
-          qu = fma(K.dt3, zR[0][y_r], qs[cc]);
+          qu = fma(K.dt3, zk[y_r], qs[cc]);
 #pragma unroll
           for (int f = 1; f <= 4; ++f) Qv[f] = qs[f * C1 + cc];
           yu = qs[5 * C1 + cc];
@@ -397,33 +409,36 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
         cglob += L.plane;
-        __syncwarp();
-        if (lane == 0) {
-          if (B) mbar_arrive(qempty + nq % G::RQ);
-          mbar_arrive(pempty + psl2);  // P plane k
-        }
-        if (B) ++nq;
-      } else if (jj < 2) {
-        // planes kb-2, kb-1 never reach the second stage: free their P slots now
-        __syncwarp();
-        if (lane == 0) mbar_arrive(pempty + psl);
       }
+      // ---- release what this warp has finished reading
       __syncwarp();
-      if (lane == 0) mbar_arrive(zempty + zsl[0]);  // input plane p - 2
-      // advance the rings: input planes shift by one, P slot of plane p+1, of plane p-1
+      if (lane == 0) {
+        if (B && second) mbar_arrive(qempty + nq % G::RQ);
+        if (B) {
+          if (first) mbar_arrive(pempty + psl);          // P plane p (first stage only)
+        } else if (second) {
+          mbar_arrive(pempty + pslk);                     // P plane k
+        } else if (jj < 2) {
+          mbar_arrive(pempty + psl);                      // planes kb-2, kb-1: no second stage
+        }
+        if (jj >= 1) mbar_arrive(zempty + zsl[0]);        // input plane p - 3
+      }
+      if (B && second) ++nq;
+      // ---- advance the rings
 #pragma unroll
-      for (int q = 0; q < 4; ++q) zsl[q] = zsl[q + 1];
-      zsl[4] = zsl[3] + 1 == G::RZ ? 0 : zsl[3] + 1;
-      if (zsl[4] == 0) zph ^= 1;
-      // P slot of plane (p+1)-2 for the next iteration: ring index p0 + jj - 1
-      psl2 = (jj == 1) ? (int)(p0 % G::RP) : (psl2 + 1 == G::RP ? 0 : psl2 + 1);
+      for (int q = 0; q < 5; ++q) zsl[q] = zsl[q + 1];
+      zsl[5] = zsl[4] + 1 == G::RZ ? 0 : zsl[4] + 1;
+      if (zsl[5] == 0) zph ^= 1;
+      if (jj == 2) pslk = (int)(p0 % G::RP);            // plane k of iteration 3 = P index 0
+      else if (jj > 2) pslk = pslk + 1 == G::RP ? 0 : pslk + 1;
       psl = psl + 1 == G::RP ? 0 : psl + 1;
       if (psl == 0) pph ^= 1;
     }
-    // the last two P planes (ke, ke+1) and input planes ke .. ke+3 were only read
+    // input planes ke .. ke+3 and (A) P planes ke, ke+1 were only read
     __syncwarp();
     if (lane == 0) {
-      for (int q = 0; q < 2; ++q) mbar_arrive(pempty + (p0 + nk + 2 + q) % G::RP);
+      if (!B)
+        for (int q = 0; q < 2; ++q) mbar_arrive(pempty + (p0 + nk + 2 + q) % G::RP);
       for (int q = 0; q < 4; ++q) mbar_arrive(zempty + (z0 + nk + 4 + q) % G::RZ);
     }
     nz = z0 + nk + 8;
