@@ -57,11 +57,13 @@ def measured_traffic(config: str, variant: int):
     return None if t is None else t.get("dram_bytes_per_step")
 
 
-def bssn_fp64_roofline(pts: int, step_s: float):
+def bssn_fp64_roofline(pts: int, step_s: float, variant: int):
     """fp64-pipe roofline for the BSSN step: thread-level fp64 instructions per point-update
-    (ncu sm__inst_executed_pipe_fp64 x 32 / points, committed in profiles/r1_traffic.json)
-    vs 148 SMs x 64 fp64 lanes x the max SM clock."""
-    t = _traffic_table().get("bssn192", {}).get("fp64_thread_instr_per_point_step")
+    of this kernel design (ncu sm__inst_executed_pipe_fp64 x 32 / points, committed in
+    profiles/r1_traffic.json) vs 148 SMs x 64 fp64 lanes x the max SM clock."""
+    tab = _traffic_table().get("bssn192", {})
+    t = tab.get(str(variant), {}).get("fp64_thread_instr_per_point_step") or \
+        tab.get("fp64_thread_instr_per_point_step")
     if not t:
         return {}
     peak_inst = 148 * 64 * 1.965e9  # fp64 thread-instructions / s at max clock (DFMA = 2 flops)
@@ -288,15 +290,15 @@ def main():
                 "frac_of_nominal_8TBps": achieved / 8000.0}
     # our kernel launches per RK4 step: wave 2 (stage pairs) or 4 (one per stage); BSSN
     # 4 (two-phase table kernel, variant 0, or fused single kernel, 1) or 3 fissioned
-    # groups x 4 stages (variant 2)
+    # groups x 4 stages (variant 2), or derivative + 2 algebra kernels x 4 stages (variant 3)
     if cfg["system"] == "wave":
         launches_per_step = 2 if variant == 6 else 4
     else:
-        launches_per_step = 12 if variant == 2 else 4
+        launches_per_step = 12 if variant in (2, 3) else 4
     if cfg["system"] == "bssn":
         # BSSN is bound by the fp64 pipe: fp64 instructions per point-update
         # counted by ncu (profiles/r1_traffic.json) against 64 DFMA lanes/SM/clock.
-        roofline.update(bssn_fp64_roofline(pts_local, mean_step_s))
+        roofline.update(bssn_fp64_roofline(pts_local, mean_step_s, variant))
 
     # e2e through the public API with host buffers: per step, upload the state from pinned
     # host memory, one RK4 step, download the state.

@@ -796,6 +796,174 @@ __global__ void __launch_bounds__(64) bssn_tab(StageLaunch a, BssnK K, double* r
   }
 }
 
+// ------------------------------------------------------------------ derivative table in HBM
+// Variant 3: the kernel fission of PAPER.md:537-547 taken to the derivative/algebra
+// boundary.  A stencil-only kernel writes the 136 derivative slots of every interior point
+// (45 D1, 66 second derivatives, 25 advection terms; the layout of the SMEM table above
+// minus the point values) to an HBM table [slot][point]; the algebra kernels then read point
+// values from the stage input and derivatives from the table -- pointwise and coalesced, so
+// the register-heavy algebra has no stencil loads in flight.  Table traffic: 136 x 8 B
+// written + read per point per stage.
+constexpr int NTAB = NSLOT - T_D1;            // 136
+// Derivative kernel: one CTA per (32 x 8 tile, z chunk, GF).  It marches the chunk with an
+// 8-plane shared-memory ring of the GF's planes (tile + 3-point halo), so every stencil
+// operand is read from HBM/L2 once per CTA, and writes all table slots of that GF (D1 if
+// differentiated, the 6 second derivatives if twice differentiated, the advection term)
+// with streaming stores.  Same operation order as StencilP (D1raw, D2raw, D11raw, ADVraw).
+constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 * DR, DPL = DSX * DSY;
+constexpr int DZC = 16, DRING = 8;
+
+template <int STAGE>
+__global__ void __launch_bounds__(256) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
+  __shared__ double ring[DRING][DPL];
+  const Layout& L = a.L;
+  const int gf = blockIdx.y;
+  const int t = blockIdx.x;
+  const int bx = t % ntx, by = (t / ntx) % nty, ch = t / (ntx * nty);
+  const int i0 = bx * DT_X, j0 = by * DT_Y;
+  const int kb = a.k_begin + ch * DZC, ke = min(kb + DZC, a.k_end);
+  const double* in = stage_input<STAGE>(a);
+  const double* f = in + gf * L.gfs;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int i = i0 + tx, j = j0 + ty;
+  const bool live = i < L.nx && j < L.ny;
+  const int64_t ni = L.nx * L.ny * L.nz;
+  const int xmax = (int)L.nx + L.g - 1, ymax = (int)L.ny + L.g - 1;
+  auto load = [&](int plane) {
+    double* dst = ring[(plane + DRING) & (DRING - 1)];
+    for (int e = threadIdx.x; e < DPL; e += 256) {
+      const int x = min(i0 - DR + e % DSX, xmax), y = min(j0 - DR + e / DSX, ymax);
+      dst[e] = ld(f + L.idx(x, y, plane));
+    }
+  };
+  const int e1 = d1i(gf), e2 = ddi(gf);
+  for (int q = -DR; q < DR; ++q) load(kb + q);
+  const int c = (ty + DR) * DSX + tx + DR;
+  double* tab = a.dtab;
+  for (int k = kb; k < ke; ++k) {
+    load(k + DR);
+    __syncthreads();
+    if (live) {
+      auto F = [&](int dx, int dy, int dz) { return ring[(k + dz + DRING) & (DRING - 1)][c + dy * DSX + dx]; };
+      auto D1 = [&](int ax, int ox, int oy, int oz) {  // D1raw along axis ax at offset (ox,oy,oz)
+        const int sx = ax == 0, sy_ = ax == 1, sz = ax == 2;
+        return 8.0 * (F(ox + sx, oy + sy_, oz + sz) - F(ox - sx, oy - sy_, oz - sz)) -
+               (F(ox + 2 * sx, oy + 2 * sy_, oz + 2 * sz) - F(ox - 2 * sx, oy - 2 * sy_, oz - 2 * sz));
+      };
+      const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
+      const double f0 = F(0, 0, 0);
+      if (e1 >= 0) {
+#pragma unroll
+        for (int l = 0; l < 3; ++l) __stcs(tab + (3 * e1 + l) * ni + o, D1(l, 0, 0, 0) * K.i12h[l]);
+      }
+      if (e2 >= 0) {
+        double* tt = tab + (45 + 6 * e2) * ni + o;
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+          const int l = sI(p), m = sJ(p);
+          double v;
+          if (l == m) {
+            const int sx = l == 0, sy_ = l == 1, sz = l == 2;
+            v = (16.0 * (F(sx, sy_, sz) + F(-sx, -sy_, -sz)) - (F(2 * sx, 2 * sy_, 2 * sz) + F(-2 * sx, -2 * sy_, -2 * sz)) -
+                 30.0 * f0) * K.i12h2[l];
+          } else {
+            const int sx = l == 0, sy_ = l == 1, sz = l == 2;
+            const double p1 = D1(m, sx, sy_, sz), m1 = D1(m, -sx, -sy_, -sz);
+            const double p2 = D1(m, 2 * sx, 2 * sy_, 2 * sz), m2 = D1(m, -2 * sx, -2 * sy_, -2 * sz);
+            v = (8.0 * (p1 - m1) - (p2 - m2)) * K.i144hh[l + m - 1];
+          }
+          __stcs(tt + p * ni, v);
+        }
+      }
+      const int64_t cg = L.idx(i, j, k);
+      double r = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int sx = q == 0, sy_ = q == 1, sz = q == 2;
+        const double beta = ld(in + (V_BETA + q) * L.gfs + cg);
+        const double a1 = F(sx, sy_, sz), b1 = F(-sx, -sy_, -sz);
+        const double a2 = F(2 * sx, 2 * sy_, 2 * sz), b2 = F(-2 * sx, -2 * sy_, -2 * sz);
+        const double a3 = F(3 * sx, 3 * sy_, 3 * sz), b3 = F(-3 * sx, -3 * sy_, -3 * sz);
+        const double S = 21.0 * (a1 - b1) - 6.0 * (a2 - b2) + (a3 - b3);
+        const double A = 15.0 * (a1 + b1) - 6.0 * (a2 + b2) + (a3 + b3) - 20.0 * f0;
+        r = fma(fma(beta, S, fabs(beta) * A), K.i24h[q], r);
+      }
+      __stcs(tab + (111 + gf) * ni + o, r);
+    }
+  }
+}
+
+struct HbmP {
+  const double* in;
+  int64_t gfs, c;
+  const double* tab;
+  int64_t ni, o;
+  __device__ __forceinline__ double v(int gf) const { return ld(in + gf * gfs + c); }
+  __device__ __forceinline__ double d1(const BssnK&, int gf, int l) const {
+    return __ldcs(tab + (3 * d1i(gf) + l) * ni + o);
+  }
+  __device__ __forceinline__ double dd(const BssnK&, int gf, int l, int m, double) const {
+    return __ldcs(tab + (45 + 6 * ddi(gf) + sy(l, m)) * ni + o);
+  }
+  __device__ __forceinline__ double adv(const BssnK&, int gf, const double*, double) const {
+    return __ldcs(tab + (111 + gf) * ni + o);
+  }
+};
+
+template <int STAGE, int G, int MB>
+__global__ void __launch_bounds__(128, MB) bssn_alg(StageLaunch a, BssnK K, double* rhs_dst) {
+  const Layout& L = a.L;
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 4 + threadIdx.y;
+  const int k = a.k_begin + blockIdx.z;
+  if (i >= L.nx || j >= L.ny) return;
+  const int64_t c = L.idx(i, j, k);
+  const double* in = stage_input<STAGE>(a);
+  HbmP P{in, L.gfs, c, a.dtab, L.nx * L.ny * L.nz, (int64_t(k) * L.ny + j) * L.nx + i};
+  double r[NV];
+  bssn_point<G>(P, K, r);
+  bssn_update<STAGE, G>(a, K, r, in, c, i, j, k, rhs_dst);
+}
+
+template <int STAGE>
+cudaError_t launch_hbm(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  if (!a.dtab) return cudaErrorInvalidValue;
+  const dim3 block(32, 4, 1);
+  const unsigned gx = (unsigned)((a.L.nx + 31) / 32), gy = (unsigned)((a.L.ny + 3) / 4);
+  {
+    const int ntx = (int)((a.L.nx + DT_X - 1) / DT_X), nty = (int)((a.L.ny + DT_Y - 1) / DT_Y);
+    const int nch = (nk + DZC - 1) / DZC;
+    bssn_deriv<STAGE><<<dim3((unsigned)(ntx * nty * nch), NV, 1), 256, 0, st>>>(a, K, ntx, nty);
+  }
+  // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM for the algebra kernels (register cap)
+  static int mb = -1;
+  if (mb < 0) {
+    const char* e = getenv("CHEMORA_BSSN_ALG_MB");
+    mb = e ? atoi(e) : 3;
+  }
+  const dim3 grid(gx, gy, (unsigned)nk);
+  switch (mb) {
+    case 2:
+      bssn_alg<STAGE, 2, 2><<<grid, block, 0, st>>>(a, K, dst);
+      bssn_alg<STAGE, 13, 2><<<grid, block, 0, st>>>(a, K, dst);
+      break;
+    case 3:
+      bssn_alg<STAGE, 2, 3><<<grid, block, 0, st>>>(a, K, dst);
+      bssn_alg<STAGE, 13, 3><<<grid, block, 0, st>>>(a, K, dst);
+      break;
+    case 4:
+      bssn_alg<STAGE, 2, 4><<<grid, block, 0, st>>>(a, K, dst);
+      bssn_alg<STAGE, 13, 4><<<grid, block, 0, st>>>(a, K, dst);
+      break;
+    default:
+      bssn_alg<STAGE, 2, 1><<<grid, block, 0, st>>>(a, K, dst);
+      bssn_alg<STAGE, 13, 1><<<grid, block, 0, st>>>(a, K, dst);
+  }
+  return cudaGetLastError();
+}
+
 template <int STAGE, int G>
 cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
@@ -827,9 +995,10 @@ cudaError_t launch_tab(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
 
 template <int STAGE>
 cudaError_t launch_stage(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
-  // variant 0 (default): two-phase table kernel; 1: fused single kernel (stencils from
-  // global memory); 2: the fissioned kernels G1, G2, G3
+  // variant 0: two-phase SMEM table kernel; 1: fused single kernel (stencils from global
+  // memory); 2: the fissioned kernels G1, G2, G3; 3: HBM derivative table + algebra kernels
   if (a.variant == 1) return launch<STAGE, 0>(a, K, dst, st);
+  if (a.variant == 3) return launch_hbm<STAGE>(a, K, dst, st);
   if (a.variant == 2) {
     cudaError_t e = launch<STAGE, 1>(a, K, dst, st);
     if (e == cudaSuccess) e = launch<STAGE, 2>(a, K, dst, st);

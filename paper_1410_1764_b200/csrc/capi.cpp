@@ -74,6 +74,7 @@ struct chemora_grid_s {
   double* mon_partials;
   int64_t mon_n;
   double* mon_hist;             // ring of kMonHist per-step energies (device)
+  double* dtab;                 // BSSN derivative table (kBssnTab x interior points) or null
   uint64_t mon_written;         // steps recorded since creation
   uint64_t mon_read;            // steps already returned by chemora_read_monitor
 };
@@ -134,8 +135,9 @@ size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 // workspace: [sets][norm scratch][norm out][params][flags]
 constexpr int kMonHist = 1024;  // energy-monitor ring (steps)
+constexpr int kBssnTab = 136;   // BSSN derivative-table slots per point (bssn_stage.cu variant 3)
 struct WsPlan {
-  size_t sets, scratch, out, params, flags, mon, hist, total;
+  size_t sets, scratch, out, params, flags, mon, hist, tab, total;
   int64_t mon_n;
 };
 WsPlan plan_ws(const Layout& L, int system) {
@@ -162,6 +164,9 @@ WsPlan plan_ws(const Layout& L, int system) {
   off += align256(sizeof(double) * (size_t)p.mon_n);
   p.hist = off;
   off += align256(sizeof(double) * kMonHist);
+  // BSSN: HBM derivative table of the table-fission kernels, [slot][interior point]
+  p.tab = off;
+  if (system == CHEMORA_SYS_BSSN) off += align256(sizeof(double) * (size_t)kBssnTab * L.nx * L.ny * L.nz);
   p.total = off;
   return p;
 }
@@ -271,6 +276,7 @@ StageLaunch stage_args(chemora_grid_t g, double dt) {
   a.variant = g->variant;
   a.band = g->band;
   a.mon_partials = nullptr;
+  a.dtab = g->dtab;
   return a;
 }
 
@@ -380,6 +386,7 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->norm_scratch = reinterpret_cast<double*>(g->ws + P.scratch);
   g->norm_out = reinterpret_cast<double*>(g->ws + P.out);
   g->dparams = reinterpret_cast<double*>(g->ws + P.params);
+  g->dtab = g->desc.system == CHEMORA_SYS_BSSN ? reinterpret_cast<double*>(g->ws + P.tab) : nullptr;
   g->monitor = false;
   g->mon_partials = reinterpret_cast<double*>(g->ws + P.mon);
   g->mon_n = P.mon_n;
@@ -400,7 +407,8 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->cur = 0;
   // default tiling: the temporally blocked stage pairs for 4th-order wave grids (fastest
   // measured, profiles/r1_wave_design_study.md), else one thread per point; BSSN: fission
-  g->variant = desc->system == CHEMORA_SYS_BSSN ? 2 /* fissioned G1/G2/G3 */
+  // at the derivative/algebra boundary through the HBM table (fastest measured at 192^3)
+  g->variant = desc->system == CHEMORA_SYS_BSSN ? 3 /* HBM derivative table */
              : (desc->fd_order == 0 || desc->fd_order == 4) ? kVariantFused : 0;
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
@@ -634,6 +642,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
   } else {
     cands.push_back({0, 0});
     cands.push_back({2, 0});  // fissioned one-thread-per-point kernels
+    cands.push_back({3, 0});  // HBM derivative table + algebra kernels
     if (g->L.nx * g->L.ny * g->L.nz <= (int64_t)64 * 64 * 64) cands.push_back({1, 0});
   }
   const int saved_v = g->variant, saved_b = g->band;

@@ -38,6 +38,7 @@ struct StageLaunch {
   int variant;           // kernel variant (0 = default fast, 1 = simple reference kernel)
   int band;              // wave simple-kernel CTA band order (-1 auto, 0 plain 3-D order)
   double* mon_partials;  // NEXT-3 fused energy monitor: per-CTA partials of stage 4 (or null)
+  double* dtab;          // BSSN variant 3: HBM derivative table [136][interior point]
 };
 
 // Wave (Eq. 1) -------------------------------------------------------------------------
