@@ -811,14 +811,17 @@ constexpr int NTAB = NSLOT - T_D1;            // 136
 // differentiated, the 6 second derivatives if twice differentiated, the advection term)
 // with streaming stores.  Same operation order as StencilP (D1raw, D2raw, D11raw, ADVraw).
 constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 * DR, DPL = DSX * DSY;
-constexpr int DZC = 16, DRING = 8;
+constexpr int DZC = 16, DRING = 8, DNT = DT_X * DT_Y;
 
 template <int STAGE>
-__global__ void __launch_bounds__(256) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
-  __shared__ double ring[DRING][DPL];
+__global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
+  extern __shared__ __align__(16) double dring[];
+  double (*ring)[DPL] = reinterpret_cast<double (*)[DPL]>(dring);
+  double* gzb = dring + DRING * DPL;   // D1raw_z f on the whole plane (tile + halo)
+  double* gyb = gzb + DPL;             // D1raw_y f on the tile rows, all DSX columns
   const Layout& L = a.L;
-  const int gf = blockIdx.y;
-  const int t = blockIdx.x;
+  const int gf = blockIdx.x;  // GFs fastest: the 25 CTAs of a tile run together (beta from L2)
+  const int t = blockIdx.y;
   const int bx = t % ntx, by = (t / ntx) % nty, ch = t / (ntx * nty);
   const int i0 = bx * DT_X, j0 = by * DT_Y;
   const int kb = a.k_begin + ch * DZC, ke = min(kb + DZC, a.k_end);
@@ -829,20 +832,38 @@ __global__ void __launch_bounds__(256) bssn_deriv(StageLaunch a, BssnK K, int nt
   const bool live = i < L.nx && j < L.ny;
   const int64_t ni = L.nx * L.ny * L.nz;
   const int xmax = (int)L.nx + L.g - 1, ymax = (int)L.ny + L.g - 1;
+  // asynchronous plane copies (cp.async, one commit group per plane): the copy of plane
+  // k + 4 overlaps the computation of plane k
   auto load = [&](int plane) {
     double* dst = ring[(plane + DRING) & (DRING - 1)];
-    for (int e = threadIdx.x; e < DPL; e += 256) {
+    for (int e = threadIdx.x; e < DPL; e += DNT) {
       const int x = min(i0 - DR + e % DSX, xmax), y = min(j0 - DR + e / DSX, ymax);
-      dst[e] = ld(f + L.idx(x, y, plane));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + e)),
+                   "l"(f + L.idx(x, y, plane))
+                   : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   const int e1 = d1i(gf), e2 = ddi(gf);
-  for (int q = -DR; q < DR; ++q) load(kb + q);
+  for (int q = -DR; q <= DR; ++q) load(kb + q);
   const int c = (ty + DR) * DSX + tx + DR;
   double* tab = a.dtab;
   for (int k = kb; k < ke; ++k) {
-    load(k + DR);
-    __syncthreads();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // plane k + 3 has landed
+    __syncthreads();  // ... for every thread, and plane k - 4's slot is no longer read
+    if (k + DR + 1 < ke + DR) load(k + DR + 1);
+    if (e2 >= 0) {
+      // inner derivatives of the mixed second derivatives, shared by the tile: D1_z on the
+      // plane (for d_x d_z at x-halo columns and d_y d_z at y-halo rows), D1_y on the rows
+      auto Fr = [&](int e, int dz) { return ring[(k + dz + DRING) & (DRING - 1)][e]; };
+      for (int e = threadIdx.x; e < DPL; e += DNT)
+        gzb[e] = 8.0 * (Fr(e, 1) - Fr(e, -1)) - (Fr(e, 2) - Fr(e, -2));
+      for (int e = threadIdx.x; e < DT_Y * DSX; e += DNT) {
+        const int q = e + DR * DSX;
+        gyb[e] = 8.0 * (Fr(q + DSX, 0) - Fr(q - DSX, 0)) - (Fr(q + 2 * DSX, 0) - Fr(q - 2 * DSX, 0));
+      }
+      __syncthreads();
+    }
     if (live) {
       auto F = [&](int dx, int dy, int dz) { return ring[(k + dz + DRING) & (DRING - 1)][c + dy * DSX + dx]; };
       auto D1 = [&](int ax, int ox, int oy, int oz) {  // D1raw along axis ax at offset (ox,oy,oz)
@@ -867,9 +888,10 @@ __global__ void __launch_bounds__(256) bssn_deriv(StageLaunch a, BssnK K, int nt
             v = (16.0 * (F(sx, sy_, sz) + F(-sx, -sy_, -sz)) - (F(2 * sx, 2 * sy_, 2 * sz) + F(-2 * sx, -2 * sy_, -2 * sz)) -
                  30.0 * f0) * K.i12h2[l];
           } else {
-            const int sx = l == 0, sy_ = l == 1, sz = l == 2;
-            const double p1 = D1(m, sx, sy_, sz), m1 = D1(m, -sx, -sy_, -sz);
-            const double p2 = D1(m, 2 * sx, 2 * sy_, 2 * sz), m2 = D1(m, -2 * sx, -2 * sy_, -2 * sz);
+            // outer D1 along l of the inner D1raw along m, read from the shared buffers
+            const double* gb = (m == 1) ? gyb + ty * DSX + tx + DR : gzb + c;
+            const int so = (l == 0) ? 1 : DSX;   // (l, m) = (x, y), (x, z) or (y, z)
+            const double p1 = gb[so], m1 = gb[-so], p2 = gb[2 * so], m2 = gb[-2 * so];
             v = (8.0 * (p1 - m1) - (p2 - m2)) * K.i144hh[l + m - 1];
           }
           __stcs(tt + p * ni, v);
@@ -935,7 +957,13 @@ cudaError_t launch_hbm(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
   {
     const int ntx = (int)((a.L.nx + DT_X - 1) / DT_X), nty = (int)((a.L.ny + DT_Y - 1) / DT_Y);
     const int nch = (nk + DZC - 1) / DZC;
-    bssn_deriv<STAGE><<<dim3((unsigned)(ntx * nty * nch), NV, 1), 256, 0, st>>>(a, K, ntx, nty);
+    constexpr int smem = (DRING * DPL + DPL + DT_Y * DSX) * 8;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(bssn_deriv<STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    bssn_deriv<STAGE><<<dim3(NV, (unsigned)(ntx * nty * nch), 1), DNT, smem, st>>>(a, K, ntx, nty);
   }
   // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM for the algebra kernels (register cap)
   static int mb = -1;
