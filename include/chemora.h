@@ -64,7 +64,11 @@ enum chemora_init {
                                    kind_params = {A, W} or NULL for {1, 0.5}                 */
   CHEMORA_INIT_NOISE = 4,       /* every GF = SplitMix64(seed ^ (gf<<40 + I)) -> [-1,1),
                                    I = global interior index i + Nx (j + Ny k)               */
-  CHEMORA_INIT_MINK_PERT = 5    /* BSSN: flat + seeded sines, kind_params = {eps} or NULL   */
+  CHEMORA_INIT_MINK_PERT = 5,   /* BSSN: flat + seeded sines, kind_params = {eps} or NULL   */
+  CHEMORA_INIT_GAUGE_WAVE = 6   /* BSSN: the gauge-wave exact solution at time t (SURVEY.md
+                                   App. A.3), H = 1 - amp sin(2 pi (x + s t - t)/d),
+                                   constant shift beta^x = s; kind_params = {amp, d, s, t} or
+                                   NULL for {0.1, 1, 0, 0}; needs |amp| < 1, d > 0        */
 };
 
 /* Grid descriptor (SPEC.md:415-418 UniformGrid). */

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libchemora.so")
 
 SYS_WAVE, SYS_BSSN = 1, 2
 N_GF = {SYS_WAVE: 5, SYS_BSSN: 25}
-INIT_HOST, INIT_HOST_PADDED, INIT_PLANE_WAVES, INIT_GAUSSIAN, INIT_NOISE, INIT_MINK_PERT = range(6)
+INIT_HOST, INIT_HOST_PADDED, INIT_PLANE_WAVES, INIT_GAUSSIAN, INIT_NOISE, INIT_MINK_PERT, INIT_GAUGE_WAVE = range(7)
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_PEER",
           6: "E_NONFINITE", 7: "E_UNSUPPORTED"}
 E_NONFINITE = 6

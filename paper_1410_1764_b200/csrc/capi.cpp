@@ -481,9 +481,10 @@ static int set_initial_nofill(chemora_grid_t g, int kind, const double* host_src
       if (g->desc.system != CHEMORA_SYS_WAVE) return fail(CHEMORA_E_INVALID, "init kind needs the wave system");
       /* fallthrough */
     case CHEMORA_INIT_NOISE:
-    case CHEMORA_INIT_MINK_PERT: {
-      if (kind == CHEMORA_INIT_MINK_PERT && g->desc.system != CHEMORA_SYS_BSSN)
-        return fail(CHEMORA_E_INVALID, "MINK_PERT needs the BSSN system");
+    case CHEMORA_INIT_MINK_PERT:
+    case CHEMORA_INIT_GAUGE_WAVE: {
+      if ((kind == CHEMORA_INIT_MINK_PERT || kind == CHEMORA_INIT_GAUGE_WAVE) && g->desc.system != CHEMORA_SYS_BSSN)
+        return fail(CHEMORA_E_INVALID, "MINK_PERT / GAUGE_WAVE need the BSSN system");
       InitArgs a;
       memset(&a, 0, sizeof(a));
       a.kind = kind;
@@ -497,6 +498,12 @@ static int set_initial_nofill(chemora_grid_t g, int kind, const double* host_src
       }
       if (kind == CHEMORA_INIT_GAUSSIAN) { a.kp[0] = kp ? kp[0] : 1.0; a.kp[1] = kp ? kp[1] : 0.5; }
       if (kind == CHEMORA_INIT_MINK_PERT) a.kp[0] = kp ? kp[0] : 1e-3;
+      if (kind == CHEMORA_INIT_GAUGE_WAVE) {
+        const double def[4] = {0.1, 1.0, 0.0, 0.0};
+        for (int q = 0; q < 4; ++q) a.kp[q] = kp ? kp[q] : def[q];
+        if (!(std::fabs(a.kp[0]) < 1.0) || !(a.kp[1] > 0.0))
+          return fail(CHEMORA_E_INVALID, "GAUGE_WAVE needs |amp| < 1 and d > 0");
+      }
       CUDA_TRY(cudaMemsetAsync(g->sets.y - L.c0, 0, sizeof(double) * L.gfs * L.n_gf, st));
       CUDA_TRY(init_interior(L, g->sets.y, a, st));
       break;

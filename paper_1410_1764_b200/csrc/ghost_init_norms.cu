@@ -114,6 +114,29 @@ __global__ void init_kernel(Layout L, double* set, InitArgs a) {
     set[1 * L.gfs + c] = A * exp(-0.5 * r2 / (Wd * Wd));
     return;
   }
+  if (a.kind == 6) {  // GAUGE_WAVE (BSSN), kp = {amp, d, shift, t}
+    const double amp = a.kp[0], d = a.kp[1], shift = a.kp[2], t = a.kp[3];
+    const double pi2 = 6.283185307179586476925286766559;
+    const double ph = pi2 * (x + shift * t - t) / d;
+    double s, cs;
+    sincos(ph, &s, &cs);
+    const double H = 1.0 - amp * s;
+    const double dHdt = amp * (pi2 / d) * cs, dHdx = -amp * (pi2 / d) * cs;
+    const double Kxx = -dHdt / (2.0 * sqrt(H));
+    for (int f = 0; f < nf; ++f) set[f * L.gfs + c] = 0.0;
+    set[0 * L.gfs + c] = log(H) / 12.0;
+    set[1 * L.gfs + c] = pow(H, 2.0 / 3.0);
+    set[4 * L.gfs + c] = pow(H, -1.0 / 3.0);
+    set[6 * L.gfs + c] = pow(H, -1.0 / 3.0);
+    set[7 * L.gfs + c] = Kxx / H;
+    set[8 * L.gfs + c] = (2.0 / 3.0) * pow(H, -1.0 / 3.0) * Kxx;
+    set[11 * L.gfs + c] = -(1.0 / 3.0) * pow(H, -4.0 / 3.0) * Kxx;
+    set[13 * L.gfs + c] = -(1.0 / 3.0) * pow(H, -4.0 / 3.0) * Kxx;
+    set[14 * L.gfs + c] = (2.0 / 3.0) * pow(H, -5.0 / 3.0) * dHdx;
+    set[17 * L.gfs + c] = sqrt(H);
+    set[19 * L.gfs + c] = shift;
+    return;
+  }
   if (a.kind == 5) {  // MINK_PERT (BSSN)
     const double eps = a.kp[0];
     const double len = a.gext[0] * a.h[0];
