@@ -483,7 +483,16 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
   static int nsm = 0;
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
-  int nchunks = (nk + 63) / 64;
+  // z planes per item (CHEMORA_FUSED_CHUNK, default 128 -- measured best of 32..512 at 512^3):
+  // longer chunks recompute fewer halo
+  // planes, shorter ones balance the persistent CTAs better
+  static int zc = 0;
+  if (!zc) {
+    const char* e = getenv("CHEMORA_FUSED_CHUNK");
+    zc = e ? atoi(e) : 128;
+    if (zc < 4) zc = 64;
+  }
+  int nchunks = (nk + zc - 1) / zc;
   const int want = (8 * nsm + ntx * nty - 1) / (ntx * nty);
   if (nchunks < want) nchunks = want;
   int chunk = (nk + nchunks - 1) / nchunks;
