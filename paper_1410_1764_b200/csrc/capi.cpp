@@ -38,6 +38,8 @@ constexpr int kParams = 10;
 
 struct PeerRecord {
   cudaIpcMemHandle_t handle;
+  uint64_t offset;   // workspace offset inside the exported allocation (caching allocators
+                     // may place it inside a larger cudaMalloc block; the handle maps the base)
   uint64_t bytes;
   int32_t rank, nranks;
   int64_t local_extent[3];
@@ -219,6 +221,22 @@ typedef CUresult (*PFN_wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 typedef CUresult (*PFN_write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 PFN_wait64 g_wait64 = nullptr;
 PFN_write64 g_write64 = nullptr;
+typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+// Base of the allocation that contains p (cuMemGetAddressRange), 0 if unavailable.
+uint64_t allocation_base(const void* p) {
+  static PFN_range fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f) return 0;
+    fn = reinterpret_cast<PFN_range>(f);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) return 0;
+  return (uint64_t)base;
+}
+
 int load_stream_memops() {
   if (g_wait64 && g_write64) return CHEMORA_OK;
   cudaDriverEntryPointQueryResult q1, q2;
@@ -886,6 +904,9 @@ int chemora_grid_export_peer(chemora_grid_t g, void* rec_out) {
   PeerRecord rec;
   memset(&rec, 0, sizeof(rec));
   CUDA_TRY(cudaIpcGetMemHandle(&rec.handle, g->ws));
+  const uint64_t base = allocation_base(g->ws);
+  if (!base) return fail(CHEMORA_E_PEER, "cuMemGetAddressRange failed for the workspace");
+  rec.offset = (uint64_t)(uintptr_t)g->ws - base;
   rec.bytes = g->ws_bytes;
   rec.rank = g->desc.rank;
   rec.nranks = g->desc.nranks;
@@ -916,7 +937,7 @@ int chemora_grid_connect_ipc(chemora_grid_t g, const void* rlo, const void* rhi)
     cudaError_t e = cudaIpcOpenMemHandle(&p, rec.handle, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return fail(CHEMORA_E_PEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
     g->opened.push_back(p);
-    *base = static_cast<char*>(p);
+    *base = static_cast<char*>(p) + rec.offset;
     return CHEMORA_OK;
   };
   char* blo = nullptr;
