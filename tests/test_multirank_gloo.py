@@ -111,6 +111,33 @@ def test_norm_partials_combine_in_rank_order(world):
             assert col[rr] == pytest.approx((field[0, z0:z0 + nz] ** 2).sum(), rel=1e-14)
 
 
+def _constraints(rank, world):
+    """Constraint-monitor partials [sum c^2, max |c|] x 7 of each rank's slab, gathered and
+    combined on every rank (the host half of Grid.constraint_norms for nranks > 1)."""
+    from paper_1410_1764_b200 import dist as D
+    rng = np.random.default_rng(7)
+    c = rng.standard_normal((7, 12, 5, 6))
+    z0, nz = D.slab_bounds(12, world, rank)
+    sl = c[:, z0:z0 + nz]
+    part = np.zeros(14)
+    for q in range(7):
+        part[2 * q] = (sl[q] ** 2).sum()
+        part[2 * q + 1] = np.abs(sl[q]).max()
+    gathered = D.gather_partials(part, world)
+    return D.combine_constraint_partials(gathered, 0.25).tolist()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_constraint_partials_combine(world):
+    res = _run(world, "_constraints")
+    c = np.random.default_rng(7).standard_normal((7, 12, 5, 6))
+    for r in range(world):
+        assert res[r] == res[0]
+        for q in range(7):
+            assert res[r][2 * q] == pytest.approx(np.sqrt(0.25 * (c[q] ** 2).sum()), rel=1e-14)
+            assert res[r][2 * q + 1] == np.abs(c[q]).max()
+
+
 def test_slab_bounds_and_validation():
     from paper_1410_1764_b200 import capi as C
     from paper_1410_1764_b200 import dist as D
