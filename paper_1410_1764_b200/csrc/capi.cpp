@@ -304,11 +304,17 @@ cudaError_t launch_stage(chemora_grid_t g, const StageLaunch& a, int stage, cuda
 
 // Temporally blocked wave step (wave_fused.cu): two kernels per step, the new state lands
 // in the scratch set, which then becomes the state set.
-constexpr int kVariantFused = 6;
+// Variant 6: 32x8 tiles (wave_fused.cu); variant 7: 32x16 tiles, two rows per thread
+// (wave_fused2.cu).
+constexpr int kVariantFused = 6, kVariantFused2 = 7;
+bool is_fused_variant(int v) { return v == kVariantFused || v == kVariantFused2; }
 bool use_fused(chemora_grid_t g) {
   const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
-  return g->desc.system == CHEMORA_SYS_WAVE && g->variant == kVariantFused && order == 4 && !g->monitor &&
+  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 && !g->monitor &&
          g->L.g >= 4;
+}
+cudaError_t fused_pair(int variant, const StageLaunch& a, int pair, cudaStream_t st) {
+  return variant == kVariantFused2 ? wave_fused2_pair(a, pair, st) : wave_fused_pair(a, pair, st);
 }
 void swap_state(chemora_grid_t g) {
   std::swap(g->sets.y, g->sets.b);
@@ -466,7 +472,7 @@ int chemora_grid_local(chemora_grid_t g, int64_t* ext, int64_t* z0) {
 int chemora_get_kernel_variant(chemora_grid_t g, int* variant) {
   if (int rc = check_grid(g)) return rc;
   if (!variant) return fail(CHEMORA_E_INVALID, "variant is NULL");
-  *variant = use_fused(g) ? kVariantFused : (g->variant == kVariantFused ? 0 : g->variant);
+  *variant = use_fused(g) ? g->variant : (is_fused_variant(g->variant) ? 0 : g->variant);
   return CHEMORA_OK;
 }
 
@@ -616,7 +622,7 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
       for (int pair = 0; pair < 2; ++pair) {
         if (2 * pair + 2 > dbg_stop) return CHEMORA_OK;
         if (int rc = phase_wait(g, st)) return rc;
-        CUDA_TRY(wave_fused_pair(a, pair, st));
+        CUDA_TRY(fused_pair(g->variant, a, pair, st));
         if (int rc = phase_signal(g, st)) return rc;
       }
       swap_state(g);
@@ -652,18 +658,23 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
   cudaStream_t st = as_stream(stream);
   // candidate tilings (variant, band), pruned by a footprint model:
   //   wave: one thread per point in plain order (L1/L2 reuse of every stencil operand),
-  //         the same in the banded L2-window order, and the persistent TMA z-march (only
-  //         when its 32x16 tiles fill the SMs and the stencil radius is <= 2);
+  //         the persistent TMA z-march (only when its 32x16 tiles fill the SMs and the
+  //         stencil radius is <= 2), and for 4th order the two temporally blocked pair
+  //         kernels (32x8 and 32x16 tiles), else the banded L2-window order;
   //   BSSN: fissioned kernels, and the fused single kernel only for small grids (it spills).
   struct Cand { int variant, band; };
   std::vector<Cand> cands;
   if (g->desc.system == CHEMORA_SYS_WAVE) {
     cands.push_back({0, 0});
-    cands.push_back({0, -1});
     const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     if (order <= 4 && tiles >= 148) cands.push_back({4, 0});
-    if (order == 4 && g->L.g >= 4 && !g->monitor) cands.push_back({kVariantFused, 0});
+    if (order == 4 && g->L.g >= 4 && !g->monitor) {
+      cands.push_back({kVariantFused, 0});
+      cands.push_back({kVariantFused2, 0});
+    } else {
+      cands.push_back({0, -1});
+    }
   } else {
     cands.push_back({0, 0});
     cands.push_back({2, 0});  // fissioned one-thread-per-point kernels
@@ -685,12 +696,12 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     // bytes (120 vs 112 B/pt); the temporally blocked candidate times both pair kernels
     // (its new state lands in B and is not rotated in).
     StageLaunch a = stage_args(g, 0.0);
-    const bool fusedc = cands[c].variant == kVariantFused;
+    const bool fusedc = is_fused_variant(cands[c].variant);
     auto run = [&](float* ms3) -> cudaError_t {
       cudaError_t e = cudaSuccess;
       if (fusedc) {
-        e = wave_fused_pair(a, 0, st);
-        if (e == cudaSuccess) e = wave_fused_pair(a, 1, st);
+        e = fused_pair(cands[c].variant, a, 0, st);
+        if (e == cudaSuccess) e = fused_pair(cands[c].variant, a, 1, st);
         return e;
       }
       const int last = g->desc.system == CHEMORA_SYS_WAVE ? 3 : 1;
@@ -770,7 +781,7 @@ int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t 
       for (int pair = 0; pair < 2; ++pair)
         for (int r = 0; r < n; ++r) {
           StageLaunch a = stage_args(grids[r], dt);
-          CUDA_TRY(wave_fused_pair(a, pair, st));
+          CUDA_TRY(fused_pair(grids[r]->variant, a, pair, st));
         }
       for (int r = 0; r < n; ++r) swap_state(grids[r]);
     } else {

@@ -47,6 +47,8 @@ cudaError_t wave_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
 // temporally blocked stage pairs (wave_fused.cu): pair 0 = stages 1+2, pair 1 = stages 3+4
 // (new state into the scratch set s.b); fd_order 4, storage ghost >= 4
 cudaError_t wave_fused_pair(const StageLaunch& a, int pair, cudaStream_t st);
+// variant 7 (wave_fused2.cu): the same pairs on 32x16 tiles, two output rows per thread
+cudaError_t wave_fused2_pair(const StageLaunch& a, int pair, cudaStream_t st);
 // persistent TMA z-march (wave_tma.cu), fd_order 2 or 4, stages 1..4
 cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st);
 

@@ -1,6 +1,7 @@
-"""GPU tests of the temporally blocked wave step (wave_fused.cu, kernel variant 6): stages
-1+2 and 3+4 each in one kernel with the intermediate state kept in shared memory.  It must
-give bit-identical states to the one-kernel-per-stage path and match the oracle."""
+"""GPU tests of the temporally blocked wave step (kernel variants 6, wave_fused.cu, 32x8
+tiles, and 7, wave_fused2.cu, 32x16 tiles with two rows per thread): stages 1+2 and 3+4
+each in one kernel with the intermediate state kept in shared memory.  They must give
+bit-identical states to the one-kernel-per-stage path and match the oracle."""
 from __future__ import annotations
 
 import math
@@ -13,6 +14,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 FUSED = 6
+FUSED_VARIANTS = [6, 7]
 
 
 def _mods():
@@ -34,23 +36,26 @@ def _run(n, variant, steps, seed=2, ghost=3):
     return g, h
 
 
-@pytest.mark.parametrize("n", [(70, 45, 33), (64, 64, 64), (33, 17, 40), (8, 8, 8)])
+@pytest.mark.parametrize("fv", FUSED_VARIANTS)
+@pytest.mark.parametrize("n", [(70, 45, 33), (64, 64, 64), (33, 17, 40), (8, 8, 8), (40, 37, 20)])
 @pytest.mark.parametrize("steps", [1, 2, 3])
-def test_fused_bitwise_equal_to_stagewise(n, steps):
+def test_fused_bitwise_equal_to_stagewise(n, steps, fv):
     a, _ = _run(n, 0, steps)
-    b, _ = _run(n, FUSED, steps)
+    b, _ = _run(n, fv, steps)
     assert np.array_equal(a.get_state(), b.get_state())
     assert np.array_equal(a.get_state(padded=True), b.get_state(padded=True))
 
 
-def test_fused_parity_10_steps():
+@pytest.mark.parametrize("fv", FUSED_VARIANTS)
+def test_fused_parity_10_steps(fv):
     n = (48, 40, 56)
     P, C = _mods()
     h = tuple(2 * math.pi / v for v in n)
     dt = 0.25 * min(h)
     y0 = ci.pw3(n, h)
     g = P.Grid(C.SYS_WAVE, n, h)
-    g.set_kernel_variant(FUSED)
+    g.set_kernel_variant(fv)
+    assert g.kernel_variant() == fv
     g.set_initial(C.INIT_HOST, y0)
     g.rk4_step(dt, 10)
     ref = oracle.rk4(oracle.WAVE, y0, h, dt, 10)
@@ -61,12 +66,13 @@ def test_fused_parity_10_steps():
     np.testing.assert_allclose(g.norms(), nref, rtol=1e-12, atol=1e-12 * np.abs(nref).max())
 
 
-def test_fused_ghosts_and_variant_switch():
+@pytest.mark.parametrize("fv", FUSED_VARIANTS)
+def test_fused_ghosts_and_variant_switch(fv):
     """Ghosts of the (rotated) state set are the periodic fill; switching back to the
     stage-wise kernels mid-run continues from the right set."""
     n = (40, 24, 32)
     a, h = _run(n, 0, 5)
-    b, _ = _run(n, FUSED, 3)
+    b, _ = _run(n, fv, 3)
     b.set_kernel_variant(0)
     b.rk4_step(0.25 * min(h), 2)
     assert np.array_equal(a.get_state(), b.get_state())
@@ -75,8 +81,9 @@ def test_fused_ghosts_and_variant_switch():
     assert np.array_equal(pad, ref)
 
 
+@pytest.mark.parametrize("fv", FUSED_VARIANTS)
 @pytest.mark.parametrize("nslabs", [2, 4])
-def test_fused_local_slabs(nslabs):
+def test_fused_local_slabs(nslabs, fv):
     P, C = _mods()
     n = (36, 20, 64)
     h = tuple(2 * math.pi / v for v in n)
@@ -86,20 +93,21 @@ def test_fused_local_slabs(nslabs):
     g.rk4_step(0.25 * min(h), 3)
     s = P.LocalSlabs(C.SYS_WAVE, n, h, nslabs)
     for gg in s.grids:
-        gg.set_kernel_variant(FUSED)
+        gg.set_kernel_variant(fv)
     s.set_initial(C.INIT_HOST, y0)
     s.rk4_step(0.25 * min(h), 3)
     assert np.array_equal(s.get_state(), g.get_state())
 
 
-def test_fused_nonfinite_reported():
+@pytest.mark.parametrize("fv", FUSED_VARIANTS)
+def test_fused_nonfinite_reported(fv):
     P, C = _mods()
     n = (16, 16, 16)
     h = (2 * math.pi / 16,) * 3
     y0 = ci.noise(n, 5, seed=1)
     y0[3, 4, 5, 6] = np.inf
     g = P.Grid(C.SYS_WAVE, n, h)
-    g.set_kernel_variant(FUSED)
+    g.set_kernel_variant(fv)
     g.set_initial(C.INIT_HOST, y0)
     g.rk4_step(0.1, 2)
     with pytest.raises(C.ChemoraError) as ei:
