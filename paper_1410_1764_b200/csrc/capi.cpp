@@ -310,8 +310,9 @@ constexpr int kVariantFused = 6, kVariantFused2 = 7;
 bool is_fused_variant(int v) { return v == kVariantFused || v == kVariantFused2; }
 bool use_fused(chemora_grid_t g) {
   const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
-  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 && !g->monitor &&
-         g->L.g >= 4;
+  // the energy monitor is fused into variant 6's kernel B (not into variant 7)
+  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 &&
+         !(g->monitor && g->variant != kVariantFused) && g->L.g >= 4;
 }
 cudaError_t fused_pair(int variant, const StageLaunch& a, int pair, cudaStream_t st) {
   return variant == kVariantFused2 ? wave_fused2_pair(a, pair, st) : wave_fused_pair(a, pair, st);
@@ -622,7 +623,15 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
       for (int pair = 0; pair < 2; ++pair) {
         if (2 * pair + 2 > dbg_stop) return CHEMORA_OK;
         if (int rc = phase_wait(g, st)) return rc;
+        if (pair == 1 && mon) {
+          CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
+          a.mon_partials = g->mon_partials;
+        }
         CUDA_TRY(fused_pair(g->variant, a, pair, st));
+        if (pair == 1 && mon) {
+          CUDA_TRY(monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st));
+          g->mon_written += 1;
+        }
         if (int rc = phase_signal(g, st)) return rc;
       }
       swap_state(g);
@@ -669,9 +678,9 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     if (order <= 4 && tiles >= 148) cands.push_back({4, 0});
-    if (order == 4 && g->L.g >= 4 && !g->monitor) {
+    if (order == 4 && g->L.g >= 4) {
       cands.push_back({kVariantFused, 0});
-      cands.push_back({kVariantFused2, 0});
+      if (!g->monitor) cands.push_back({kVariantFused2, 0});
     } else {
       cands.push_back({0, -1});
     }

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr int OFF_PD = G::OFF_P / 8, OFF_QD = G::OFF_Q / 8, OFF_IZD = G::OFF_IZ / 8, OFF_IPD = G::OFF_IP / 8;
   constexpr int PYR = PY_R / 8, PY1 = PY_1 / 8, PY2 = PY_2 / 8;
 
+  double eacc = 0.0;  // this thread's energy sum (B, monitor on), in a fixed point order
   uint32_t nz = 0, np = 0, nq = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
@@ -399,13 +400,16 @@ __global__ void __launch_bounds__(NT, 1)
             double* outy = a.s.b;  // the new state goes to the scratch set (swapped by the caller)
             const FaceDst fd = a.img[0];
             const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
+            double esq = 0.0;  // rho^2 + v.v of the new state (fused energy monitor)
             auto put = [&](int f, double v) {
               outy[f * gfs + c] = v;
               if (nf) store_images(outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
               check_finite(a.nan_flag, code0 + f, v);
+              if (f >= 1) esq += v * v;
             };
             auto putq = [&](int, double) {};
             wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            eacc += 0.5 * esq;
           }
         }
         cglob += L.plane;
@@ -443,6 +447,21 @@ __global__ void __launch_bounds__(NT, 1)
     }
     nz = z0 + nk + 8;
     np = p0 + nk + 4;
+  }
+  // NEXT-3 fused energy monitor (Fig. 1 "Energy"): one partial per CTA,
+  // fixed shuffle tree then warps in order, so the per-step energy is deterministic
+  if (B && a.mon_partials) {
+    __shared__ double red[NCW];
+    double v = eacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    cbar();
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < NCW; ++w) sum += red[w];
+      a.mon_partials[blockIdx.x] = sum;
+    }
   }
 }
 

@@ -24,18 +24,22 @@ def _mods():
     return P, C
 
 
+@pytest.mark.parametrize("variant", [0, 6])
 @pytest.mark.parametrize("n", [(32, 32, 32), (70, 45, 33)])
-def test_fused_energy_monitor_matches_oracle(n):
-    """Energy of the state after every step, reduced inside the stage-4 kernel, equals the
-    oracle's energy of the oracle's state (1e-12) and the stand-alone norm (1e-13);
-    the state itself is bitwise unchanged by monitoring."""
+def test_fused_energy_monitor_matches_oracle(n, variant):
+    """Energy of the state after every step, reduced inside the kernel that writes the new
+    state (stage-4 kernel, variant 0; stage-pair kernel B, variant 6), equals the oracle's
+    energy of the oracle's state (1e-12) and the stand-alone norm (1e-13); the state itself
+    is bitwise unchanged by monitoring."""
     P, C = _mods()
     h = tuple(2 * math.pi / v for v in n)
     dt = 0.25 * min(h)
     y0 = ci.noise(n, 5, seed=21)
     g = P.Grid(C.SYS_WAVE, n, h)
+    g.set_kernel_variant(variant)
     g.set_initial(C.INIT_HOST, y0)
     g.set_monitor(True)
+    assert g.kernel_variant() == variant
     g.rk4_step(dt, 4)
     e = g.read_monitor()
     assert len(e) == 4
