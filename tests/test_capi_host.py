@@ -130,3 +130,17 @@ def test_combine_constraint_partials():
     out = D.combine_constraint_partials(parts.ravel(), 0.125)
     assert np.allclose(out[0::2], np.sqrt(0.125 * 3.0 * (np.arange(7) + 1.0)), rtol=1e-15)
     assert np.array_equal(out[1::2], np.maximum(0.5, np.linspace(0.1, 0.9, 7)))
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """Without libchemora.so the binding refuses to import (there is no CPU fallback)."""
+    import shutil
+    import subprocess
+    import sys
+    src = os.path.join(ROOT, "paper_1410_1764_b200")
+    shutil.copytree(src, tmp_path / "paper_1410_1764_b200",
+                    ignore=shutil.ignore_patterns("*.so", "build_obj", "csrc", "__pycache__"))
+    r = subprocess.run([sys.executable, "-c", "import paper_1410_1764_b200.capi"], cwd=tmp_path,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "is missing" in r.stderr and "no CPU fallback" in r.stderr
