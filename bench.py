@@ -197,6 +197,20 @@ def workload(args):
                            "192^3 fp64 per GPU, periodic, 3 ghost zones, fused RHS+RK4 (configs[2])",
                            "grid": list(n), "ghost": 3, "fd_order": 4, "init": "MINK_PERT eps=1e-3",
                            "l2": "state (6.2 GB) larger than L2; no flush needed"}}
+    if args.config == "wave1024":
+        n = (1024, 1024, 1024)
+        return {"system": "wave", "n": n, "strong": True,
+                "config": {"workload": "scalar wave eq (Eq. 1), 4th-order FD, 1024^3 fp64 global, "
+                           "z-slabs over the GPUs (strong scaling, configs[3]; needs >= 2 GPUs)",
+                           "grid": list(n), "ghost": 3, "fd_order": 4, "init": "PW3 plane waves",
+                           "l2": "state larger than L2; no flush needed"}}
+    if args.config == "bssn384":
+        n = (384, 384, 384)
+        return {"system": "bssn", "n": n,
+                "config": {"workload": "BSSN-like 25-GF Einstein RHS with upwinded advection, "
+                           "384^3 fp64 per GPU (weak scaling, configs[4])",
+                           "grid": list(n), "ghost": 3, "fd_order": 4, "init": "MINK_PERT eps=1e-3",
+                           "l2": "state larger than L2; no flush needed"}}
     raise SystemExit(f"unknown config {args.config}")
 
 
@@ -206,7 +220,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chemora", choices=["chemora", "reference"])
-    ap.add_argument("--config", default="wave512", choices=["wave512", "bssn192"])
+    ap.add_argument("--config", default="wave512", choices=["wave512", "bssn192", "wave1024", "bssn384"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--variant", type=int, default=None, help="stage-kernel variant (testing)")
@@ -229,7 +243,11 @@ def main():
     cfg = workload(args)
     n = cfg["n"]
     system = C.SYS_WAVE if cfg["system"] == "wave" else C.SYS_BSSN
-    gext = (n[0], n[1], n[2] * world)
+    strong = cfg.get("strong", False)
+    if strong and (world < 2 or n[2] % world):
+        raise SystemExit(f"{args.config} is a strong-scaling config for 2/4/8 GPUs (z divisible by N)")
+    # weak scaling: n per GPU, the global z extent grows with N; strong: n is the global grid
+    gext = (n[0], n[1], n[2]) if strong else (n[0], n[1], n[2] * world)
     L = 2 * math.pi if system == C.SYS_WAVE else 1.0
     h = (L / n[0], L / n[1], L / n[2])
     dt = 0.25 * min(h)
@@ -264,7 +282,7 @@ def main():
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    pts_local = n[0] * n[1] * n[2]
+    pts_local = n[0] * n[1] * (n[2] // world if strong else n[2])
     value = pts_local * world * args.steps / (total_ms * 1e-3)
 
     # roofline of the dominant kernel(s): the kernels of one RK4 step are the only launches in
@@ -337,7 +355,7 @@ def main():
         cfgout["global_grid"] = list(gext)
         line = {"metric": METRIC, "value": value, "unit": "grid-point updates/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": cfgout, "roofline": roofline, "cpu_baseline": cb,
                 "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
                 "step_ms": step_ms}
