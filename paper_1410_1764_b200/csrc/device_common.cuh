@@ -46,6 +46,29 @@ __device__ __forceinline__ void store_images(double* own, double* zlo, double* z
   store_images_n(own, zlo, zhi, (int)L.nx, (int)L.ny, (int)L.nz, L.g, L.px, L.plane, i, j, k, v);
 }
 
+// Where the periodic ghost images of a point go: `general` -- near a z face (images may go
+// to a neighbour slab) or on an x-y edge: the noinline store_images path; `single` -- near
+// exactly one x or y face: one image in the same plane at offset `off` from the point.
+struct ImageSite {
+  bool general, single;
+  int64_t off;
+};
+__device__ __forceinline__ ImageSite image_site(const Layout& L, int i, int j, int k) {
+  const int g = L.g;
+  const bool nxf = i < g || i >= L.nx - g, nyf = j < g || j >= L.ny - g;
+  ImageSite s;
+  s.general = k < g || k >= L.nz - g || (nxf && nyf);
+  s.single = nxf || nyf;
+  s.off = nxf ? (int64_t)(i < g ? L.nx : -L.nx) : (int64_t)(j < g ? L.ny : -L.ny) * L.px;
+  return s;
+}
+// Store the images of value v of one GF (own: that GF's base, c = L.idx(i, j, k)).
+__device__ __forceinline__ void put_images(const ImageSite& s, double* own, double* zlo, double* zhi,
+                                           const Layout& L, int i, int j, int k, int64_t c, double v) {
+  if (s.general) store_images(own, zlo, zhi, L, i, j, k, v);
+  else if (s.single) own[c + s.off] = v;
+}
+
 __device__ __forceinline__ bool near_face(const Layout& L, int i, int j, int k) {
   const int g = L.g;
   return i < g || j < g || k < g || i >= L.nx - g || j >= L.ny - g || k >= L.nz - g;

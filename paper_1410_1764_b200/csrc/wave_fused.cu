@@ -386,21 +386,15 @@ __global__ void __launch_bounds__(NT, 1)
         }
         if (live) {
           const int64_t c = cglob;
-          // periodic ghost images: a point near exactly one x or y face (the common case:
-          // the edge lanes of the x-edge tiles, the edge rows of the y-edge tiles) has one
-          // image in the same plane at i -/+ nx or j -/+ ny -- stored inline; points near a z
-          // face (images may go to a neighbour slab) or an x-y edge take the general path
-          const bool nxf = i < g || i >= L.nx - g, nyf = j < g || j >= L.ny - g;
-          const bool nf = k < g || k >= L.nz - g || (nxf && nyf);
-          const bool n1 = nxf || nyf;
-          const int64_t xim = nxf ? (i < g ? L.nx : -L.nx) : (j < g ? L.ny : -L.ny) * L.px;
+          // periodic ghost images: one inline store for a point near exactly one x or y
+          // face, the general noinline path for z faces and edges (device_common.cuh)
+          const ImageSite isite = image_site(L, i, j, k);
           if (!B) {
             double* outc = a.s.c;
             const FaceDst fd = a.img[1];
             auto put = [&](int f, double v) {
               outc[f * gfs + c] = v;
-              if (nf) store_images(outc + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
-              else if (n1) outc[f * gfs + c + xim] = v;
+              put_images(isite, outc + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
             };
             auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
             wave_update<2>(K, S, kk, Y, Qv, yu, qu, put, putq);
@@ -411,8 +405,7 @@ __global__ void __launch_bounds__(NT, 1)
             double esq = 0.0;  // rho^2 + v.v of the new state (fused energy monitor)
             auto put = [&](int f, double v) {
               outy[f * gfs + c] = v;
-              if (nf) store_images(outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, v);
-              else if (n1) outy[f * gfs + c + xim] = v;
+              put_images(isite, outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
               check_finite(a.nan_flag, code0 + f, v);
               if (f >= 1) esq += v * v;
             };
