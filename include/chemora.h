@@ -226,12 +226,17 @@ int chemora_autotune(chemora_grid_t grid, int32_t trials, int32_t* chosen, doubl
 
 /* ---- testing hooks (not part of the user-facing contract) */
 
-/* Select the stage-kernel variant of this handle: 0 = tiled fast kernel (default),
- * 1 = one-thread-per-point reference kernel.  Results must be bitwise identical. */
+/* Select the kernel design of this handle.  WAVE: 0 = one thread per point,
+ * 1 = same in plain order, 2 = register z-march, 3/4 = TMA z-marches, 5 = SMEM brick (one
+ * kernel per RK stage), 6 = temporally blocked stage pairs on 32x8 tiles (default for 4th
+ * order), 7 = the same on 32x16 tiles; every wave design is bitwise identical.  BSSN: 0 =
+ * two-phase SMEM table, 1 = fused single kernel, 2 = fissioned G1/G2/G3, 3 = HBM derivative
+ * table + algebra kernels (default); results agree to rounding. */
 int chemora_set_kernel_variant(chemora_grid_t grid, int variant);
 
-/* The stage-kernel variant that chemora_rk4_step will run for this handle (6 = temporally
- * blocked stage pairs, 0-5 = one kernel per stage in various tilings). */
+/* The kernel design chemora_rk4_step will run for this handle (a temporally blocked variant
+ * falls back to 0 where it does not apply: fd_order != 4, ghost storage < 4, variant 7 with
+ * the energy monitor on). */
 int chemora_get_kernel_variant(chemora_grid_t grid, int* variant);
 
 /* Copy state set `set` (0 = y, 1 = Q, 2 = B, 3 = C, in the current rotation) padded to host
