@@ -848,9 +848,15 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
   for (int q = -DR; q <= DR; ++q) load(kb + q);
   const int c = (ty + DR) * DSX + tx + DR;
   double* tab = a.dtab;
+  double zq[2 * DR + 1];  // this thread's column at planes k-3 .. k+3 (z stencils from registers)
   for (int k = kb; k < ke; ++k) {
     asm volatile("cp.async.wait_group 0;" ::: "memory");  // plane k + 3 has landed
     __syncthreads();  // ... for every thread, and plane k - 4's slot is no longer read
+    if (k == kb) {
+#pragma unroll
+      for (int q = 0; q < 2 * DR; ++q) zq[q] = ring[(k - DR + q + DRING) & (DRING - 1)][c];
+    }
+    zq[2 * DR] = ring[(k + DR + DRING) & (DRING - 1)][c];
     if (k + DR + 1 < ke + DR) load(k + DR + 1);
     if (e2 >= 0) {
       // inner derivatives of the mixed second derivatives, shared by the tile: D1_z on the
@@ -865,7 +871,9 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
       __syncthreads();
     }
     if (live) {
-      auto F = [&](int dx, int dy, int dz) { return ring[(k + dz + DRING) & (DRING - 1)][c + dy * DSX + dx]; };
+      auto F = [&](int dx, int dy, int dz) {
+        return (dx == 0 && dy == 0) ? zq[dz + DR] : ring[(k + dz + DRING) & (DRING - 1)][c + dy * DSX + dx];
+      };
       auto D1 = [&](int ax, int ox, int oy, int oz) {  // D1raw along axis ax at offset (ox,oy,oz)
         const int sx = ax == 0, sy_ = ax == 1, sz = ax == 2;
         return 8.0 * (F(ox + sx, oy + sy_, oz + sz) - F(ox - sx, oy - sy_, oz - sz)) -
@@ -912,6 +920,8 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
       }
       __stcs(tab + (111 + gf) * ni + o, r);
     }
+#pragma unroll
+    for (int q = 0; q < 2 * DR; ++q) zq[q] = zq[q + 1];
   }
 }
 
