@@ -243,3 +243,22 @@ def test_fd_order_parity(order):
         assert relerr(k, oracle.rhs(W, y0, h, g=4, order=order)) <= 1e-13
         g.rk4_step(dt, 10)
         assert relerr(g.get_state(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", [0, 6])
+def test_zero_steps_is_a_noop(variant):
+    """nsteps = 0 leaves the state (ghosts included) bitwise untouched; negative nsteps and a
+    non-finite dt are rejected."""
+    P, C = _mods()
+    n = (40, 24, 32)
+    h = tuple(2 * math.pi / v for v in n)
+    g = P.Grid(C.SYS_WAVE, n, h)
+    g.set_kernel_variant(variant)
+    g.set_initial(C.INIT_NOISE, seed=5)
+    before = g.get_state(padded=True)
+    g.rk4_step(0.1, 0)
+    assert np.array_equal(g.get_state(padded=True), before)
+    with pytest.raises(C.ChemoraError):
+        g.rk4_step(0.1, -1)
+    with pytest.raises(C.ChemoraError):
+        g.rk4_step(float("nan"), 1)
