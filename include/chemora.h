@@ -125,6 +125,16 @@ int chemora_set_initial(chemora_grid_t grid, int kind, const double* host_src,
  * Returns CHEMORA_E_NONFINITE if a previous step produced NaN/Inf (data still copied). */
 int chemora_get_state(chemora_grid_t grid, double* host_dst, void* stream);
 
+/* Stream-ordered state transfer for pipelined host I/O (several grids / streams in flight):
+ * enqueue the copy of the local interior [gf][Nz_local][Ny][Nx] from / to PINNED host memory
+ * on `stream` and return without synchronising; the caller keeps the host buffer alive and
+ * unmodified until the stream has passed this point.  chemora_upload_state then fills the
+ * ghosts (chemora_halo_exchange, collective when nranks > 1) and clears the non-finite flag;
+ * unlike chemora_set_initial it does not reset the step counter or clear the pad.  Non-finite
+ * values surface at the next chemora_get_state / chemora_norms*. */
+int chemora_upload_state(chemora_grid_t grid, const double* host_src, void* stream);
+int chemora_download_state(chemora_grid_t grid, double* host_dst, void* stream);
+
 /* As chemora_get_state but padded [gf][Nz_local+2g][Ny+2g][Nx+2g], ghosts included. */
 int chemora_get_state_padded(chemora_grid_t grid, double* host_dst, void* stream);
 

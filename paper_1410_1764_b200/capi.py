@@ -56,6 +56,8 @@ _SIGS = {
     "chemora_set_initial_nofill": ([_vp, ctypes.c_int, _dp, _dp, ctypes.c_uint64, _vp], ctypes.c_int),
     "chemora_get_state": ([_vp, _dp, _vp], ctypes.c_int),
     "chemora_get_state_padded": ([_vp, _dp, _vp], ctypes.c_int),
+    "chemora_upload_state": ([_vp, _vp, _vp], ctypes.c_int),
+    "chemora_download_state": ([_vp, _vp, _vp], ctypes.c_int),
     "chemora_rhs": ([_vp, _vp, _vp], ctypes.c_int),
     "chemora_rk4_step": ([_vp, ctypes.c_double, ctypes.c_int32, _vp], ctypes.c_int),
     "chemora_rk4_step_multi": ([ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_double,
@@ -168,6 +170,16 @@ def chemora_get_state(h, out: np.ndarray, stream=None, padded=False, allow_nonfi
         return rc
     _check(rc, "chemora_get_state")
     return rc
+
+
+def chemora_upload_state(h, host_ptr: int, stream=None):
+    """Stream-ordered upload from pinned host memory (address `host_ptr`), then ghost fill."""
+    _check(_lib.chemora_upload_state(h, _vp(host_ptr), stream), "chemora_upload_state")
+
+
+def chemora_download_state(h, host_ptr: int, stream=None):
+    """Stream-ordered download to pinned host memory (address `host_ptr`); no synchronisation."""
+    _check(_lib.chemora_download_state(h, _vp(host_ptr), stream), "chemora_download_state")
 
 
 def chemora_rhs(h, dev_dst_ptr: int, stream=None):

@@ -583,6 +583,31 @@ int chemora_debug_get_set(chemora_grid_t g, int set, double* host, void* stream)
   return rc;
 }
 
+int chemora_upload_state(chemora_grid_t g, const double* host, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!host) return fail(CHEMORA_E_INVALID, "host_src is NULL");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  for (int f = 0; f < g->L.n_gf; ++f) {
+    cudaMemcpy3DParms p = copy_params(g, f, const_cast<double*>(host), true, false);
+    CUDA_TRY(cudaMemcpy3DAsync(&p, st));
+  }
+  CUDA_TRY(cudaMemsetAsync(g->nan_flag, 0xFF, sizeof(unsigned long long), st));  // = ~0
+  return halo_one(g, st);
+}
+
+int chemora_download_state(chemora_grid_t g, double* host, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!host) return fail(CHEMORA_E_INVALID, "host_dst is NULL");
+  DeviceGuard dg(g->desc.device);
+  cudaStream_t st = as_stream(stream);
+  for (int f = 0; f < g->L.n_gf; ++f) {
+    cudaMemcpy3DParms p = copy_params(g, f, host, false, false);
+    CUDA_TRY(cudaMemcpy3DAsync(&p, st));
+  }
+  return CHEMORA_OK;
+}
+
 int chemora_get_state(chemora_grid_t g, double* host, void* stream) {
   return get_state_impl(g, host, stream, false);
 }

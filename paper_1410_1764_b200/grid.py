@@ -56,6 +56,18 @@ class Grid:
         C.chemora_get_state(self.handle, out, self.stream, padded, allow_nonfinite)
         return out
 
+    def upload_state(self, host: torch.Tensor):
+        """Enqueue the upload of a pinned host tensor [gf][z][y][x] on this grid's stream."""
+        assert host.is_pinned() and host.dtype == torch.float64 and host.is_contiguous()
+        assert tuple(host.shape) == self.interior_shape()
+        C.chemora_upload_state(self.handle, host.data_ptr(), self.stream)
+
+    def download_state(self, host: torch.Tensor):
+        """Enqueue the download into a pinned host tensor on this grid's stream (no sync)."""
+        assert host.is_pinned() and host.dtype == torch.float64 and host.is_contiguous()
+        assert tuple(host.shape) == self.interior_shape()
+        C.chemora_download_state(self.handle, host.data_ptr(), self.stream)
+
     def rhs(self, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = torch.empty(self.interior_shape(), dtype=torch.float64, device=self.device)

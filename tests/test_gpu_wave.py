@@ -262,3 +262,34 @@ def test_zero_steps_is_a_noop(variant):
         g.rk4_step(0.1, -1)
     with pytest.raises(C.ChemoraError):
         g.rk4_step(float("nan"), 1)
+
+
+def test_stream_ordered_upload_download():
+    """chemora_upload_state / chemora_download_state (pinned, no synchronisation) give the same
+    state, ghosts and step result as chemora_set_initial(HOST) / chemora_get_state, also with
+    two grids alternating on two streams."""
+    P, C = _mods()
+    import torch
+    n = (40, 24, 32)
+    h = tuple(2 * math.pi / v for v in n)
+    y0 = ci.noise(n, 5, seed=8)
+    ref = P.Grid(C.SYS_WAVE, n, h)
+    ref.set_initial(C.INIT_HOST, y0)
+    ref_pad0 = ref.get_state(padded=True)
+    ref.rk4_step(0.1, 1)
+    want = ref.get_state()
+    grids = [P.Grid(C.SYS_WAVE, n, h) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    hin = torch.from_numpy(y0).pin_memory()
+    outs = [torch.empty(y0.shape, dtype=torch.float64).pin_memory() for _ in range(2)]
+    for b in range(2):
+        with torch.cuda.stream(streams[b]):
+            grids[b].upload_state(hin)
+            if b == 0:
+                pad = grids[b].get_state(padded=True)
+            grids[b].rk4_step(0.1, 1)
+            grids[b].download_state(outs[b])
+    torch.cuda.synchronize()
+    assert np.array_equal(pad, ref_pad0)
+    for b in range(2):
+        assert np.array_equal(outs[b].numpy(), want)
