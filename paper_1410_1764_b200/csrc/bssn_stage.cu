@@ -811,7 +811,7 @@ constexpr int NTAB = NSLOT - T_D1;            // 136
 // differentiated, the 6 second derivatives if twice differentiated, the advection term)
 // with streaming stores.  Same operation order as StencilP (D1raw, D2raw, D11raw, ADVraw).
 constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 * DR, DPL = DSX * DSY;
-constexpr int DZC = 16, DRING = 8, DNT = DT_X * DT_Y;
+constexpr int DZC = 48, DRING = 8, DNT = DT_X * DT_Y;
 
 template <int STAGE>
 __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
