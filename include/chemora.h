@@ -195,10 +195,12 @@ int chemora_grid_connect_ipc(chemora_grid_t grid, const void* record_lo, const v
 /* ---- analysis and tuning */
 
 /* Fused energy monitor (wave only; Fig. 1 "Energy" eps = 1/2 (rho^2 + delta^ij v_i v_j),
- * PAPER.md:642-644): when enabled, the kernel of every chemora_rk4_step step that writes the
- * new state (the stage-4 kernel, or the stage-pair kernel B of the temporally blocked path)
- * also reduces E = h^3 sum eps of that state (deterministic per-CTA partials + a fixed-order
- * sum) -- no extra HBM pass over the state.  Single-slab grids (nranks == 1) only. */
+ * PAPER.md:642-644): when enabled, the kernel of every chemora_rk4_step(_multi) step that
+ * writes the new state (the stage-4 kernel, or the stage-pair kernel B of the temporally
+ * blocked path) also reduces E = h^3 sum eps of that state over the LOCAL slab
+ * (deterministic per-CTA partials + a fixed-order sum) -- no extra HBM pass over the state.
+ * With nranks > 1 the global energy is the sum of the slabs' values (the Python Grid /
+ * LocalSlabs helpers add them in rank order). */
 int chemora_set_monitor(chemora_grid_t grid, int enable);
 
 /* Copy up to max per-step energies recorded since the last read (oldest first) to out;

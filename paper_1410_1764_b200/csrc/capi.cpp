@@ -810,19 +810,38 @@ int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t 
   cudaStream_t st = as_stream(stream);
   bool fused = true;
   for (int r = 0; r < n; ++r) fused = fused && use_fused(grids[r]);
+  // per-slab fused energy monitor: the kernel that writes the new state leaves its partials,
+  // reduced into that slab's history (the global energy is the sum over slabs)
+  auto mon_on = [&](chemora_grid_t g) { return g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0; };
+  auto mon_begin = [&](chemora_grid_t g, StageLaunch& a) -> cudaError_t {
+    if (!mon_on(g)) return cudaSuccess;
+    a.mon_partials = g->mon_partials;
+    return cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st);
+  };
+  auto mon_end = [&](chemora_grid_t g) -> cudaError_t {
+    if (!mon_on(g)) return cudaSuccess;
+    const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
+    cudaError_t e = monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st);
+    g->mon_written += 1;
+    return e;
+  };
   for (int step = 0; step < nsteps; ++step) {
     if (fused) {
       for (int pair = 0; pair < 2; ++pair)
         for (int r = 0; r < n; ++r) {
           StageLaunch a = stage_args(grids[r], dt);
+          if (pair == 1) CUDA_TRY(mon_begin(grids[r], a));
           CUDA_TRY(fused_pair(grids[r]->variant, a, pair, st));
+          if (pair == 1) CUDA_TRY(mon_end(grids[r]));
         }
       for (int r = 0; r < n; ++r) swap_state(grids[r]);
     } else {
       for (int s = 1; s <= 4; ++s)
         for (int r = 0; r < n; ++r) {
           StageLaunch a = stage_args(grids[r], dt);
+          if (s == 4) CUDA_TRY(mon_begin(grids[r], a));
           CUDA_TRY(launch_stage(grids[r], a, s, st));
+          if (s == 4) CUDA_TRY(mon_end(grids[r]));
         }
     }
     for (int r = 0; r < n; ++r) grids[r]->step += 1;

@@ -50,3 +50,15 @@ def combine_constraint_partials(gathered: np.ndarray, vol: float) -> np.ndarray:
         out[2 * q] = np.sqrt(vol * s)
         out[2 * q + 1] = g[:, 2 * q + 1].max()
     return out
+
+
+def sum_in_rank_order(gathered: np.ndarray) -> np.ndarray:
+    """Rank-major [world][n] per-slab values (e.g. monitor energies) -> their sums over the
+    slabs, added in rank order (deterministic)."""
+    g = np.asarray(gathered, dtype=np.float64)
+    if g.ndim == 1:
+        g = g[:, None]
+    out = np.zeros(g.shape[1])
+    for r in range(g.shape[0]):
+        out = out + g[r]
+    return out

@@ -123,8 +123,14 @@ class Grid:
     def set_monitor(self, enable=True):
         C.chemora_set_monitor(self.handle, enable)
 
-    def read_monitor(self, max_steps=1024):
-        return C.chemora_read_monitor(self.handle, max_steps, self.stream)
+    def read_monitor(self, max_steps=1024, group=None):
+        """Per-step energies since the last read; with nranks > 1 the slab energies are
+        gathered and summed in rank order (every rank gets the global values)."""
+        e = C.chemora_read_monitor(self.handle, max_steps, self.stream)
+        if self.nranks == 1:
+            return e
+        gathered = D.gather_partials(np.asarray(e, dtype=np.float64), self.nranks, group)
+        return D.sum_in_rank_order(gathered)
 
     def autotune(self, trials=3):
         return C.chemora_autotune(self.handle, trials, self.stream)
@@ -179,6 +185,15 @@ class LocalSlabs:
     def norms(self):
         parts = np.array([C.chemora_norms_partial(g.handle, g.system, self.stream) for g in self.grids])
         return C.chemora_norms_combine(self.grids[0].desc, parts, self.nslabs)
+
+    def set_monitor(self, enable=True):
+        for g in self.grids:
+            C.chemora_set_monitor(g.handle, enable)
+
+    def read_monitor(self, max_steps=1024):
+        """Per-step global energies: the slabs' fused-monitor values summed in slab order."""
+        parts = [C.chemora_read_monitor(g.handle, max_steps, self.stream) for g in self.grids]
+        return D.sum_in_rank_order(np.array(parts, dtype=np.float64))
 
     def close(self):
         for g in self.grids:

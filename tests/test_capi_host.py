@@ -144,3 +144,13 @@ def test_missing_library_fails_loudly(tmp_path):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode != 0
     assert "is missing" in r.stderr and "no CPU fallback" in r.stderr
+
+
+def test_sum_in_rank_order():
+    """Per-slab monitor energies, rank-major -> per-step sums added in rank order."""
+    import numpy as np
+    from paper_1410_1764_b200 import dist as D
+    parts = np.array([[1.0, 2.0, 3.0], [0.5, 0.25, 0.125], [1e-17, 0.0, 1.0]])
+    out = D.sum_in_rank_order(parts)
+    assert np.array_equal(out, (parts[0] + parts[1]) + parts[2])
+    assert np.array_equal(D.sum_in_rank_order(np.array([2.0, 3.0])), np.array([5.0]))

@@ -93,3 +93,31 @@ def test_autotune_keeps_state_and_parity(system):
     ref = oracle.rk4(sysid, y0, h, dt, 2, params)
     err = max(np.abs(g.get_state()[f] - ref[f]).max() / max(np.abs(ref[f]).max(), 1e-6) for f in range(len(y0)))
     assert err <= 1e-10
+
+
+@pytest.mark.parametrize("variant", [0, 6])
+@pytest.mark.parametrize("nslabs", [2, 4])
+def test_energy_monitor_local_slabs(nslabs, variant):
+    """Per-slab fused monitors summed over the slabs (chemora_rk4_step_multi) give the
+    oracle's energy; the state is still bitwise the single-grid state."""
+    P, C = _mods()
+    n = (36, 20, 64)
+    h = tuple(2 * math.pi / v for v in n)
+    dt = 0.25 * min(h)
+    y0 = ci.noise(n, 5, seed=33)
+    s = P.LocalSlabs(C.SYS_WAVE, n, h, nslabs)
+    for g in s.grids:
+        g.set_kernel_variant(variant)
+    s.set_monitor(True)
+    s.set_initial(C.INIT_HOST, y0)
+    s.rk4_step(dt, 3)
+    e = s.read_monitor()
+    assert len(e) == 3
+    y = y0
+    for k in range(3):
+        y = oracle.rk4(oracle.WAVE, y, h, dt, 1)
+        assert e[k] == pytest.approx(oracle.norms(oracle.WAVE, y, h)[-1], rel=1e-12)
+    ref = P.Grid(C.SYS_WAVE, n, h)
+    ref.set_initial(C.INIT_HOST, y0)
+    ref.rk4_step(dt, 3)
+    assert np.array_equal(s.get_state(), ref.get_state())
