@@ -192,38 +192,50 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr int IRN = IR_X * IR_Y, I1N = I1_X * I1_Y, I2N = I2_X * I2_Y, I3N = I3_X * I3_Y;
   static_assert(IRN <= 2 * NTC && I1N <= 2 * NTC && I2N <= 2 * NTC && I3N == NTC, "tile geometry");
   // intermediate rho elements e = tid, tid + NTC: offsets into v1/v2/v3/rho(or y) boxes
-  int rR_c1[2], rR_c2[2], rR_c3[2], rR_b[2];
+  // Element -> thread map of the first stage.  Every thread has one element of each type
+  // (u = 0: e = tid); the rest is spread so the CTA barrier waits less for the busiest warp
+  // (shared loads per lane: IR 13, the others 5): the 176 extra IR elements go to warps 2-7,
+  // the 32 extra v1 elements to warp 0, the 128 extra v2 elements to warps 0-1 (two each).
+  // Busiest warp: 43 loads per lane instead of 51.
+  int rR_c1[2], rR_c2[2], rR_c3[2], rR_b[2], rR_e[2];
   bool rR_ok[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int e = tid + u * NTC;
-    rR_ok[u] = e < IRN;
+    int e = u == 0 ? tid : NTC + (tid - 64);
+    rR_ok[u] = u == 0 ? true : (tid >= 64 && tid - 64 < IRN - NTC);
+    if (!rR_ok[u]) e = IRN - 1;
+    rR_e[u] = e;
     const int x = e % IR_X, y = e / IR_X;
     rR_c1[u] = y * B1_X + x + 2;
     rR_c2[u] = (y + 2) * B2_X + x;
     rR_c3[u] = y * B3_X + x;
     rR_b[u] = (y + 2) * BR_X + x + 2;
   }
-  int r1_cr[2], r1_b[2];
+  int r1_cr[2], r1_b[2], r1_e[2];
   bool r1_ok[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int e = tid + u * NTC;
+    int e = tid + u * NTC;
     r1_ok[u] = e < I1N;
+    if (!r1_ok[u]) e = I1N - 1;
+    r1_e[u] = e;
     const int x = e % I1_X, y = e / I1_X;
     r1_cr[u] = (y + 4) * BR_X + x + 2;
     r1_b[u] = (y + 2) * B1_X + x + 2;
   }
-  int r2_cr[2], r2_b[2];
-  bool r2_ok[2];
+  int r2_cr[3], r2_b[3], r2_e[3];
+  bool r2_ok[3];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int e = tid + u * NTC;
-    r2_ok[u] = e < I2N;
+  for (int u = 0; u < 3; ++u) {
+    int e = u == 0 ? tid : NTC + (u - 1) * 64 + tid;
+    r2_ok[u] = u == 0 ? true : (tid < 64 && e < I2N);
+    if (!r2_ok[u]) e = I2N - 1;
+    r2_e[u] = e;
     const int x = e % I2_X, y = e / I2_X;
     r2_cr[u] = (y + 2) * BR_X + x + 4;
     r2_b[u] = (y + 2) * B2_X + x + 2;
   }
+  static_assert(IRN - NTC <= NTC - 64 && I1N - NTC <= 32 && I2N - NTC <= 128, "element map");
   const int r3_cr = (tid / I3_X + 4) * BR_X + tid % I3_X + 4;
   const int r3_b = (tid / I3_X + 2) * B3_X + tid % I3_X + 2;
   // second stage: this thread's point (ti, tj) of the tile
@@ -303,22 +315,22 @@ __global__ void __launch_bounds__(NT, 1)
           for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[2 + q][rR_c3[u]] - z3[2 - q][rR_c3[u]], dv3);
           dv3 = dv3 * K.ih[2];
           const double kr = dv1 + dv2 + dv3;
-          const int e = tid + u * NTC;
+          const int e = rR_e[u];
           const double base = B ? sy[e] : zR[2][rR_b[u]];
           IR[e] = fma(cdt, kr, base);
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (!r1_ok[u]) continue;
-          const int e = tid + u * NTC;
+          const int e = r1_e[u];
           const double kr = d1s_(zR[2], r1_cr[u], 1) * K.ih[0];
           const double base = B ? sy[PYR + e] : s1[r1_b[u]];
           I1[e] = fma(cdt, kr, base);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 3; ++u) {
           if (!r2_ok[u]) continue;
-          const int e = tid + u * NTC;
+          const int e = r2_e[u];
           const double kr = d1s_(zR[2], r2_cr[u], BR_X) * K.ih[1];
           const double base = B ? sy[PYR + PY1 + e] : s2[r2_b[u]];
           I2[e] = fma(cdt, kr, base);
