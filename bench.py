@@ -173,7 +173,8 @@ def run_reference(args, world, rank):
     cb, n, steps, elapsed = oracle_sample(cfg["system"], per * args.steps)
     line = {"metric": METRIC, "value": cb["value"], "unit": "grid-point updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference", "config": cfg["config"],
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "grid-point updates/s", "h2d_bytes_per_step": 0,
