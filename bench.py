@@ -68,7 +68,7 @@ def bssn_fp64_roofline(pts: int, step_s: float, variant: int):
         return {}
     peak_inst = 148 * 64 * 1.965e9  # fp64 thread-instructions / s at max clock (DFMA = 2 flops)
     achieved = t * pts / step_s
-    return {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_inst / 1e12,
+    return {"bound": "alu", "pipe": "fp64", "achieved": achieved / 1e12, "peak": peak_inst / 1e12,
             "unit": "T fp64 thread-instr/s", "frac": achieved / peak_inst,
             "fp64_instr_per_point_step": t,
             "hbm_frac_at_2400_bytes": 2400 * pts / step_s / 1e9 / measured_peaks()[0]}
