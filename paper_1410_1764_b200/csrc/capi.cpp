@@ -306,15 +306,16 @@ cudaError_t launch_stage(chemora_grid_t g, const StageLaunch& a, int stage, cuda
 // in the scratch set, which then becomes the state set.
 // Variant 6: 32x8 tiles (wave_fused.cu); variant 7: 32x16 tiles, two rows per thread
 // (wave_fused2.cu).
-constexpr int kVariantFused = 6, kVariantFused2 = 7;
-bool is_fused_variant(int v) { return v == kVariantFused || v == kVariantFused2; }
+constexpr int kVariantFused = 6, kVariantFused2 = 7, kVariantFused3 = 8;
+bool is_fused_variant(int v) { return v == kVariantFused || v == kVariantFused2 || v == kVariantFused3; }
 bool use_fused(chemora_grid_t g) {
   const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
-  // the energy monitor is fused into variant 6's kernel B (not into variant 7)
+  // the energy monitor is fused into kernel B of variants 6 and 8 (not 7)
   return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 &&
-         !(g->monitor && g->variant != kVariantFused) && g->L.g >= 4;
+         !(g->monitor && g->variant == kVariantFused2) && g->L.g >= 4;
 }
 cudaError_t fused_pair(int variant, const StageLaunch& a, int pair, cudaStream_t st) {
+  if (variant == kVariantFused3) return wave_fused3_pair(a, pair, st);
   return variant == kVariantFused2 ? wave_fused2_pair(a, pair, st) : wave_fused_pair(a, pair, st);
 }
 void swap_state(chemora_grid_t g) {

@@ -14,7 +14,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 FUSED = 6
-FUSED_VARIANTS = [6, 7]
+FUSED_VARIANTS = [6, 7, 8]
 
 
 def _mods():
