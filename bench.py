@@ -294,10 +294,12 @@ def main():
     mean_step_s = float(np.mean(step_ms)) * 1e-3
     variant = g.kernel_variant()
     floor_bpp = BYTES_PER_POINT[cfg["system"]]
-    bpp = 256 if (cfg["system"] == "wave" and variant == 6) else floor_bpp
+    pair_kernels = cfg["system"] == "wave" and variant in (6, 7, 8)   # temporally blocked pairs
+    bpp = 256 if pair_kernels else floor_bpp
     achieved = bpp * pts_local / mean_step_s / 1e9
     traffic = measured_traffic(args.config, variant)
-    kname = ("wave_fused<A>, wave_fused<B> (2 launches = 1 step)" if bpp == 256 else
+    kname = ({6: "wave_fused<A>, wave_fused<B>", 7: "wave_fused2<A>, wave_fused2<B>",
+              8: "wave_fused3<A>, wave_fused3<B>"}.get(variant, "") + " (2 launches = 1 step)" if bpp == 256 else
              "stage kernels (4 launches x groups = 1 step)")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
@@ -311,7 +313,7 @@ def main():
     # 4 (two-phase table kernel, variant 0, or fused single kernel, 1) or 3 fissioned
     # groups x 4 stages (variant 2), or derivative + 2 algebra kernels x 4 stages (variant 3)
     if cfg["system"] == "wave":
-        launches_per_step = 2 if variant == 6 else 4
+        launches_per_step = 2 if pair_kernels else 4
     else:
         launches_per_step = 12 if variant in (2, 3) else 4
     if cfg["system"] == "bssn":

@@ -431,11 +431,12 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->hi_flag = g->flags;
   g->ipc = false;
   g->cur = 0;
-  // default tiling: the temporally blocked stage pairs for 4th-order wave grids (fastest
-  // measured, profiles/r1_wave_design_study.md), else one thread per point; BSSN: fission
+  // default tiling: the temporally blocked stage pairs with register-queue z stencils for
+  // 4th-order wave grids (variant 8, fastest measured, profiles/r1_wave_design_study.md),
+  // else one thread per point; BSSN: fission
   // at the derivative/algebra boundary through the HBM table (fastest measured at 192^3)
   g->variant = desc->system == CHEMORA_SYS_BSSN ? 3 /* HBM derivative table */
-             : (desc->fd_order == 0 || desc->fd_order == 4) ? kVariantFused : 0;
+             : (desc->fd_order == 0 || desc->fd_order == 4) ? kVariantFused3 : 0;
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
@@ -706,7 +707,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     if (order <= 4 && tiles >= 148) cands.push_back({4, 0});
     if (order == 4 && g->L.g >= 4) {
       cands.push_back({kVariantFused, 0});
-      if (!g->monitor) cands.push_back({kVariantFused2, 0});
+      cands.push_back({kVariantFused3, 0});
     } else {
       cands.push_back({0, -1});
     }

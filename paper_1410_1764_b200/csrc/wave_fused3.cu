@@ -5,11 +5,10 @@
 // Every consumer thread owns one output point (ti, tj) of the 32x8 tile, and with it the
 // intermediate values at that point (rho, v1, v2, v3); the 176 / 32 / 128 halo elements of
 // the intermediate rho / v1 / v2 planes are spread over the other threads.  The thread keeps
-// in registers: the input rho and v3 at its point for planes p-2 .. p+2 and its own
-// intermediate rho and v3 for p-5 .. p-1.  All z
-// derivatives, the own-point bases and the z-neighbours of the second stage then come from
-// registers; shared memory serves only the x and y neighbours (about 30 % fewer shared loads
-// per point), and the intermediate v3 never goes to shared memory.  Same arithmetic in the
+// its own intermediate rho and v3 for planes p-5 .. p-1 in registers, so the second stage's
+// z stencils and centres need no shared loads and the intermediate v3 never goes to shared
+// memory.  (Keeping the input rho/v3 column in registers too exceeds the 168-register cap
+// of the 9-warp CTA: measured slower.)  Same arithmetic in the
 // same order as the one-kernel-per-stage path (bit-identical; no FMA contraction).
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -243,9 +242,7 @@ __global__ void __launch_bounds__(NT, 1)
     int izs[4] = {0, 0, 0, 0};                  // intermediate rho slots of planes p-3 .. p
     int ips[4] = {0, 0, 0, 0};                  // intermediate v1/v2 slots of planes p-3 .. p
     // register queues (see the file header); index 0 is the oldest plane
-    double qr[5], q3[5], qIR[5], qI3[5];   // qr/q3: input planes p-2 .. p+2
-#pragma unroll
-    for (int q = 0; q < 5; ++q) { qr[q] = 0.0; q3[q] = 0.0; }
+    double qIR[5], qI3[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) { qIR[q] = 0.0; qI3[q] = 0.0; }
 #pragma unroll 1
@@ -260,9 +257,6 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int q = 0; q < 3; ++q) ips[q] = ips[q + 1];
       ips[3] = jj % RI_P;
-      // input queues: planes p-2 .. p+2 (own point)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) { qr[q] = qr[q + 1]; q3[q] = q3[q + 1]; }
       cbar();  // the previous plane's intermediate values are complete and its reads done
       double IRown = 0.0, I3own = 0.0;
       if (first) {
@@ -275,15 +269,6 @@ __global__ void __launch_bounds__(NT, 1)
           zR[q] = sm + zsl[q + 1] * ZSD;
           z3[q] = zR[q] + ZR_D;
         }
-        if (jj == 0) {  // item start: planes p-2 .. p+1 from the ring
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            qr[q] = zR[q][o_r];
-            q3[q] = z3[q][o_3];
-          }
-        }
-        qr[4] = zR[4][o_r];
-        q3[4] = z3[4][o_3];
         const double* s1 = sm + OFF_PD + psl * PSD;
         const double* s2 = s1 + P1D;
         const double* sy = s2 + P2D;  // B only
@@ -295,11 +280,11 @@ __global__ void __launch_bounds__(NT, 1)
           const double dv1 = d1s_(s1, o_1, 1) * K.ih[0];
           const double dv2 = d1s_(s2, o_2, B2_X) * K.ih[1];
           double dv3 = 0.0;
-          dv3 = fma(C2W, q3[4] - q3[0], dv3);
-          dv3 = fma(C1W, q3[3] - q3[1], dv3);
+          dv3 = fma(C2W, z3[4][o_3] - z3[0][o_3], dv3);
+          dv3 = fma(C1W, z3[3][o_3] - z3[1][o_3], dv3);
           dv3 = dv3 * K.ih[2];
           const double kr = dv1 + dv2 + dv3;
-          const double base = B ? sy[e_R] : qr[2];
+          const double base = B ? sy[e_R] : zR[2][o_r];
           IRown = fma(cdt, kr, base);
           IR[e_R] = IRown;
         }
@@ -333,10 +318,10 @@ __global__ void __launch_bounds__(NT, 1)
         }
         {  // v3 at the own point: z neighbours of rho from the queue; stays in registers
           double dzr = 0.0;
-          dzr = fma(C2W, qr[4] - qr[0], dzr);
-          dzr = fma(C1W, qr[3] - qr[1], dzr);
+          dzr = fma(C2W, zR[4][o_r] - zR[0][o_r], dzr);
+          dzr = fma(C1W, zR[3][o_r] - zR[1][o_r], dzr);
           const double kr = dzr * K.ih[2];
-          const double base = B ? sy[PYR + PY1 + PY2 + cc] : q3[2];
+          const double base = B ? sy[PYR + PY1 + PY2 + cc] : z3[2][o_3];
           I3own = fma(cdt, kr, base);
         }
       }

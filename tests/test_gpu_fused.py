@@ -13,7 +13,6 @@ import chemora_inputs as ci
 import oracle
 
 pytestmark = pytest.mark.gpu
-FUSED = 6
 FUSED_VARIANTS = [6, 7, 8]
 
 
