@@ -814,7 +814,7 @@ constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 *
 constexpr int DZC = 48, DRING = 8, DNT = DT_X * DT_Y;
 
 template <int STAGE>
-__global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
+__global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
   extern __shared__ __align__(16) double dring[];
   double (*ring)[DPL] = reinterpret_cast<double (*)[DPL]>(dring);
   double* gzb = dring + DRING * DPL;   // D1raw_z f on the whole plane (tile + halo)
@@ -834,9 +834,9 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
   const int xmax = (int)L.nx + L.g - 1, ymax = (int)L.ny + L.g - 1;
   // asynchronous plane copies (cp.async, one commit group per plane): the copy of plane
   // k + 4 overlaps the computation of plane k
-  auto load = [&](int plane) {
+  auto load = [&](int plane) {  // always commits a group (empty past the chunk's last plane)
     double* dst = ring[(plane + DRING) & (DRING - 1)];
-    for (int e = threadIdx.x; e < DPL; e += DNT) {
+    for (int e = threadIdx.x; plane < ke + DR && e < DPL; e += DNT) {
       const int x = min(i0 - DR + e % DSX, xmax), y = min(j0 - DR + e / DSX, ymax);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + e)),
                    "l"(f + L.idx(x, y, plane))
@@ -845,19 +845,22 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   const int e1 = d1i(gf), e2 = ddi(gf);
+  // Ring use at plane k: k-2 .. k+2 (the shared D1_z of the mixed derivatives), k + 3 (the
+  // own column's z queue); so two planes can be in flight: k + 4 and k + 5 (slot of k - 3).
   for (int q = -DR; q <= DR; ++q) load(kb + q);
   const int c = (ty + DR) * DSX + tx + DR;
   double* tab = a.dtab;
   double zq[2 * DR + 1];  // this thread's column at planes k-3 .. k+3 (z stencils from registers)
-  for (int k = kb; k < ke; ++k) {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");  // plane k + 3 has landed
-    __syncthreads();  // ... for every thread, and plane k - 4's slot is no longer read
-    if (k == kb) {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
 #pragma unroll
-      for (int q = 0; q < 2 * DR; ++q) zq[q] = ring[(k - DR + q + DRING) & (DRING - 1)][c];
-    }
+  for (int q = 0; q < 2 * DR; ++q) zq[q] = ring[(kb - DR + q + DRING) & (DRING - 1)][c];
+  load(kb + DR + 1);
+  for (int k = kb; k < ke; ++k) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // plane k + 3 has landed (k + 4 may not)
+    __syncthreads();  // ... for every thread, and plane k - 3's slot is no longer read
     zq[2 * DR] = ring[(k + DR + DRING) & (DRING - 1)][c];
-    if (k + DR + 1 < ke + DR) load(k + DR + 1);
+    load(k + DR + 2);
     if (e2 >= 0) {
       // inner derivatives of the mixed second derivatives, shared by the tile: D1_z on the
       // plane (for d_x d_z at x-halo columns and d_y d_z at y-halo rows), D1_y on the rows
@@ -871,8 +874,18 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
       __syncthreads();
     }
     if (live) {
+      // the x row and y column of the own plane, read from shared memory once: the D1, D2
+      // and advection stencils of an axis share these operands, and the table stores in
+      // between would otherwise force the compiler to re-read them (generic-pointer aliasing)
+      const double* own = ring[(k + DRING) & (DRING - 1)] + c;
+      double xr[2 * DR + 1], yr[2 * DR + 1];
+#pragma unroll
+      for (int q = 0; q <= 2 * DR; ++q) {
+        xr[q] = q == DR ? zq[DR] : own[q - DR];
+        yr[q] = q == DR ? zq[DR] : own[(q - DR) * DSX];
+      }
       auto F = [&](int dx, int dy, int dz) {
-        return (dx == 0 && dy == 0) ? zq[dz + DR] : ring[(k + dz + DRING) & (DRING - 1)][c + dy * DSX + dx];
+        return (dx == 0 && dy == 0) ? zq[dz + DR] : (dy == 0 && dz == 0) ? xr[dx + DR] : yr[dy + DR];
       };
       auto D1 = [&](int ax, int ox, int oy, int oz) {  // D1raw along axis ax at offset (ox,oy,oz)
         const int sx = ax == 0, sy_ = ax == 1, sz = ax == 2;
@@ -880,6 +893,7 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
                (F(ox + 2 * sx, oy + 2 * sy_, oz + 2 * sz) - F(ox - 2 * sx, oy - 2 * sy_, oz - 2 * sz));
       };
       const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
+      const int64_t cg = L.idx(i, j, k);
       const double f0 = F(0, 0, 0);
       if (e1 >= 0) {
 #pragma unroll
@@ -905,7 +919,6 @@ __global__ void __launch_bounds__(DNT) bssn_deriv(StageLaunch a, BssnK K, int nt
           __stcs(tt + p * ni, v);
         }
       }
-      const int64_t cg = L.idx(i, j, k);
       double r = 0.0;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -968,11 +981,8 @@ cudaError_t launch_hbm(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
     const int ntx = (int)((a.L.nx + DT_X - 1) / DT_X), nty = (int)((a.L.ny + DT_Y - 1) / DT_Y);
     const int nch = (nk + DZC - 1) / DZC;
     constexpr int smem = (DRING * DPL + DPL + DT_Y * DSX) * 8;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(bssn_deriv<STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    if (cudaError_t e = smem_optin((const void*)bssn_deriv<STAGE>, smem, attr_done); e != cudaSuccess) return e;
     bssn_deriv<STAGE><<<dim3(NV, (unsigned)(ntx * nty * nch), 1), DNT, smem, st>>>(a, K, ntx, nty);
   }
   // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM for the algebra kernels (register cap)

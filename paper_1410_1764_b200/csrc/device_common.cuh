@@ -1,9 +1,33 @@
 // device_common.cuh -- small device helpers shared by the stage, ghost and init kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <cuda_runtime.h>
 #include "grid.hpp"
 
 namespace chemora {
+
+// Host helpers for the launchers.  The dynamic shared-memory opt-in is a per-device
+// attribute of a kernel, so it is recorded per (kernel, device) -- one process may drive
+// several devices -- in a bit mask owned by the call site.
+inline cudaError_t smem_optin(const void* fn, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// SM count of the current device (grid sizing of the persistent kernels).
+inline int device_sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 148;
+  return n > 0 ? n : 148;
+}
 
 // Store the periodic ghost images of interior value v at (i, j, k) (PAPER.md:345-347
 // ghost zones).  `own` is the GF array (interior-origin pointer); the

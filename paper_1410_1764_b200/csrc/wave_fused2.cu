@@ -437,16 +437,9 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
             enc(&M.v2, in, L, B2_X, B2_Y) && enc(&M.yr, a.s.y, L, IR_X, IR_Y) && enc(&M.y1, a.s.y, L, I1_X, I1_Y) &&
             enc(&M.y2, a.s.y, L, I2_X, I2_Y) && enc(&M.y3, a.s.y, L, I3_X, I3_Y);
   if (!ok) return cudaErrorInvalidValue;
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wave_fused2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_dev = dev;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = smem_optin((const void*)wave_fused2<B>, G::SMEM, attr_done); e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
   static int zc = 0;
   if (!zc) {

@@ -482,16 +482,9 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
             enc(&M.y2, a.s.y, L, I2_X, I2_Y, 1) && enc(&M.y3, a.s.y, L, I3_X, I3_Y, 1) &&
             enc(&M.q5, a.s.q, L, TX, TY, 5) && enc(&M.yu, a.s.y, L, TX, TY, 1);
   if (!ok) return cudaErrorInvalidValue;
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wave_fused3<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_dev = dev;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = smem_optin((const void*)wave_fused3<B>, G::SMEM, attr_done); e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
   // z planes per item (CHEMORA_FUSED_CHUNK, default 128 -- measured best of 32..512 at 512^3):
   // longer chunks recompute fewer halo

@@ -222,8 +222,8 @@ cudaError_t launch_zmarch(const StageLaunch& a, const WaveK& K, cudaStream_t st)
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
   const int64_t tiles = ((a.L.nx + BX - 1) / BX) * ((a.L.ny + BY - 1) / BY);
-  // enough CTAs for ~4 waves of 148 SMs x 4 resident CTAs, but chunks of >= 8 planes
-  int64_t want = (4 * 148 * 4 + tiles - 1) / tiles;
+  // enough CTAs for ~4 waves of (SMs x 4 resident CTAs), but chunks of >= 8 planes
+  int64_t want = (4 * device_sm_count() * 4 + tiles - 1) / tiles;
   int chunk = (int)((nk + want - 1) / want);
   if (chunk < 8) chunk = 8;
   if (chunk > nk) chunk = nk;
@@ -380,14 +380,8 @@ cudaError_t launch_brick(const StageLaunch& a, const WaveK& K, cudaStream_t st) 
   if (nk <= 0) return cudaSuccess;
   constexpr int RX = 32 + 2 * W, RY = 8 + 2 * W, RZ = NZ + 2 * W;
   constexpr int bytes = 8 * (RZ * RY * RX + NZ * 8 * RX + NZ * RY * 32 + RZ * 8 * 32);
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wave_brick<STAGE, W, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e != cudaSuccess) return e;
-    attr_dev = dev;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = smem_optin((const void*)wave_brick<STAGE, W, NZ>, bytes, attr_done); e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.L.nx + 31) / 32), (unsigned)((a.L.ny + 7) / 8), (unsigned)((nk + NZ - 1) / NZ));
   wave_brick<STAGE, W, NZ><<<grid, dim3(32, 8, 1), bytes, st>>>(a, K);
   return cudaGetLastError();
@@ -600,16 +594,12 @@ cudaError_t launch_tma(const StageLaunch& a, const WaveK& K, cudaStream_t st) {
       !encode_set_map(&mV2, base, L.px, L.py, L.pz, L.n_gf, L.gfs, Cf::TX, Cf::RY) ||
       !encode_set_map(&mC, base, L.px, L.py, L.pz, L.n_gf, L.gfs, Cf::TX, Cf::TY))
     return cudaErrorInvalidValue;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(wave_tma<STAGE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = smem_optin((const void*)wave_tma<STAGE, W>, Cf::SMEM, attr_done); e != cudaSuccess) return e;
   const int tiles = (int)(((L.nx + Cf::TX - 1) / Cf::TX) * ((L.ny + Cf::TY - 1) / Cf::TY));
-  // ~64-plane chunks, but at least ~8 waves of 2 CTAs x 148 SMs when the tile count is small
+  // ~64-plane chunks, but at least ~8 waves of 2 CTAs x SMs when the tile count is small
   int nchunks = (nk + 63) / 64;
-  const int want = (8 * 2 * 148 + tiles - 1) / tiles;
+  const int want = (8 * 2 * device_sm_count() + tiles - 1) / tiles;
   if (nchunks < want) nchunks = want;
   int chunk = (nk + nchunks - 1) / nchunks;
   if (chunk < 4) chunk = 4;

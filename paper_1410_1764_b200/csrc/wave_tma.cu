@@ -263,16 +263,9 @@ cudaError_t launch(const StageLaunch& a, const WaveK& K, cudaStream_t st) {
             encode(&M.y4, a.s.y, L, Cf::TX, Cf::TY, 4) && encode(&M.yu, a.s.y, L, Cf::TX, Cf::TY, 1) &&
             encode(&M.q, a.s.q, L, Cf::TX, Cf::TY, PW<STAGE>::NQ > 0 ? PW<STAGE>::NQ : 1);
   if (!ok) return cudaErrorInvalidValue;
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wave_tma2<STAGE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_dev = dev;
-  }
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = smem_optin((const void*)wave_tma2<STAGE, W>, Cf::SMEM, attr_done); e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + Cf::TX - 1) / Cf::TX), nty = (int)((L.ny + Cf::TY - 1) / Cf::TY);
   // chunks of ~64 planes, but enough items for >= 8 per SM (load balance of the round robin)
   static int chunk_env = -1;
