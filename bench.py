@@ -223,7 +223,9 @@ def main():
     ap.add_argument("--impl", default="chemora", choices=["chemora", "reference"])
     ap.add_argument("--config", default="wave512", choices=["wave512", "bssn192", "wave1024", "bssn384"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    # e2e steps: enough that the pipeline fill (first upload) and drain (last download) are
+    # amortised -- per step the two PCIe directions then overlap (scripts/pcie_probe.py)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--variant", type=int, default=None, help="stage-kernel variant (testing)")
     args = ap.parse_args()
 
@@ -330,15 +332,17 @@ def main():
     if args.e2e_steps > 0:
         shape = g.interior_shape()
         nbytes = int(np.prod(shape)) * 8
-        free, _ = torch.cuda.mem_get_info()
-        pipelined = world == 1 and free > g.nbytes + (2 << 30)
+        # on one GPU up to three grid handles take turns on their own streams, so one
+        # handle's upload, another's step and a third's download overlap (H2D engine, SMs,
+        # D2H engine); each step still moves its whole input and output over PCIe
         grids = [g]
-        if pipelined:
+        while world == 1 and len(grids) < 3 and torch.cuda.mem_get_info()[0] > g.nbytes + (2 << 30):
             g2 = P.Grid(system, gext, h, device=local, rank=rank, nranks=world)
             if args.variant is not None:
                 g2.set_kernel_variant(args.variant)
             grids.append(g2)
         nb = len(grids)
+        pipelined = nb > 1
         host_in = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(nb)]
         host_out = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(nb)]
         g.get_state(out=host_in[0].numpy())
@@ -366,9 +370,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": pts_local * world * args.e2e_steps / (e_ms * 1e-3), "unit": "grid-point updates/s",
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
                "what": ("chemora_upload_state (pinned) + chemora_rk4_step(1) + chemora_download_state per "
-                        "step" + (", two grid handles alternating on two streams" if pipelined else ""))}
+                        "step" + (f", {nb} grid handles taking turns on {nb} streams" if pipelined else ""))}
         for gg in grids[1:]:
             gg.close()
 
