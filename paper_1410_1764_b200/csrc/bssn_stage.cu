@@ -668,19 +668,32 @@ __device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K
   const FaceDst fd = a.img[STAGE - 1];
   const bool nf = near_face(L, i, j, k);
   const unsigned long long code0 = a.step * (unsigned long long)NV;
+  // all pointwise operands of the group first: the output stores below may alias them (plain
+  // pointers), so loads interleaved with the stores would serialise one memory round trip
+  // per GF
+  double p0[NV], p1[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (!in_group(G, v)) continue;
+    const int64_t o = v * gfs + c;
+    if (STAGE == 1) p0[v] = ld(in + o);
+    if (STAGE == 2) { p0[v] = ld(a.s.y + o); p1[v] = ld(in + o); }
+    if (STAGE == 3) p0[v] = ld(a.s.y + o);
+    if (STAGE == 4) { p0[v] = ld(in + o); p1[v] = ld(a.s.q + o); }
+  }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (!in_group(G, v)) continue;
     const int64_t o = v * gfs + c;
     double val;
-    if (STAGE == 1) val = fma(K.dt2, r[v], ld(in + o));
+    if (STAGE == 1) val = fma(K.dt2, r[v], p0[v]);
     if (STAGE == 2) {
-      const double yv = a.s.y[o], sv = ld(in + o);
+      const double yv = p0[v], sv = p1[v];
       a.s.q[o] = fma(K.dt3, r[v], (yv + sv) * K.third);
       val = fma(K.dt2, r[v], yv);
     }
-    if (STAGE == 3) val = fma(K.dt, r[v], a.s.y[o]);
-    if (STAGE == 4) val = fma(K.dt6, r[v], fma(ld(in + o), K.third, a.s.q[o]));
+    if (STAGE == 3) val = fma(K.dt, r[v], p0[v]);
+    if (STAGE == 4) val = fma(K.dt6, r[v], fma(p0[v], K.third, p1[v]));
     out[o] = val;
     if (nf) store_images(out + v * gfs, fd.lo + v * gfs, fd.hi + v * gfs, L, i, j, k, val);
     if (STAGE == 4) check_finite(a.nan_flag, code0 + v, val);
