@@ -847,13 +847,26 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
   const int xmax = (int)L.nx + L.g - 1, ymax = (int)L.ny + L.g - 1;
   // asynchronous plane copies (cp.async, one commit group per plane): the copy of plane
   // k + 4 overlaps the computation of plane k
+  // this thread's elements of a ring plane are the same for every plane: their in-plane
+  // offsets are computed once (the plane loop then only adds the plane base)
+  constexpr int NE = (DPL + DNT - 1) / DNT;
+  int xyo[NE];
+#pragma unroll
+  for (int m = 0; m < NE; ++m) {
+    const int e = threadIdx.x + m * DNT;
+    const int x = min(i0 - DR + e % DSX, xmax), y = min(j0 - DR + e / DSX, ymax);
+    xyo[m] = y * (int)L.px + x;
+  }
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(dring) + 8u * threadIdx.x;
   auto load = [&](int plane) {  // always commits a group (empty past the chunk's last plane)
-    double* dst = ring[(plane + DRING) & (DRING - 1)];
-    for (int e = threadIdx.x; plane < ke + DR && e < DPL; e += DNT) {
-      const int x = min(i0 - DR + e % DSX, xmax), y = min(j0 - DR + e / DSX, ymax);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + e)),
-                   "l"(f + L.idx(x, y, plane))
-                   : "memory");
+    if (plane < ke + DR) {
+      const uint32_t dst = ring_s + 8u * DPL * (uint32_t)((plane + DRING) & (DRING - 1));
+      const double* src = f + (int64_t)plane * L.plane;
+#pragma unroll
+      for (int m = 0; m < NE; ++m)
+        if (m < NE - 1 || threadIdx.x + m * DNT < DPL)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * m * DNT), "l"(src + xyo[m])
+                       : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -877,13 +890,22 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
     if (e2 >= 0) {
       // inner derivatives of the mixed second derivatives, shared by the tile: D1_z on the
       // plane (for d_x d_z at x-halo columns and d_y d_z at y-halo rows), D1_y on the rows
-      auto Fr = [&](int e, int dz) { return ring[(k + dz + DRING) & (DRING - 1)][e]; };
-      for (int e = threadIdx.x; e < DPL; e += DNT)
-        gzb[e] = 8.0 * (Fr(e, 1) - Fr(e, -1)) - (Fr(e, 2) - Fr(e, -2));
-      for (int e = threadIdx.x; e < DT_Y * DSX; e += DNT) {
-        const int q = e + DR * DSX;
-        gyb[e] = 8.0 * (Fr(q + DSX, 0) - Fr(q - DSX, 0)) - (Fr(q + 2 * DSX, 0) - Fr(q - 2 * DSX, 0));
-      }
+      const double* rm2 = ring[(k - 2 + DRING) & (DRING - 1)] + threadIdx.x;
+      const double* rm1 = ring[(k - 1 + DRING) & (DRING - 1)] + threadIdx.x;
+      const double* rp1 = ring[(k + 1 + DRING) & (DRING - 1)] + threadIdx.x;
+      const double* rp2 = ring[(k + 2 + DRING) & (DRING - 1)] + threadIdx.x;
+#pragma unroll
+      for (int m = 0; m < NE; ++m)
+        if (m < NE - 1 || threadIdx.x + m * DNT < DPL)
+          gzb[threadIdx.x + m * DNT] = 8.0 * (rp1[m * DNT] - rm1[m * DNT]) - (rp2[m * DNT] - rm2[m * DNT]);
+      const double* r0 = ring[(k + DRING) & (DRING - 1)] + DR * DSX + threadIdx.x;
+      constexpr int NEY = (DT_Y * DSX + DNT - 1) / DNT;
+#pragma unroll
+      for (int m = 0; m < NEY; ++m)
+        if (m < NEY - 1 || threadIdx.x + m * DNT < DT_Y * DSX) {
+          const double* q = r0 + m * DNT;
+          gyb[threadIdx.x + m * DNT] = 8.0 * (q[DSX] - q[-DSX]) - (q[2 * DSX] - q[-2 * DSX]);
+        }
       __syncthreads();
     }
     if (live) {
