@@ -882,6 +882,13 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
 #pragma unroll
   for (int q = 0; q < 2 * DR; ++q) zq[q] = ring[(kb - DR + q + DRING) & (DRING - 1)][c];
   load(kb + DR + 1);
+  // own-point addresses, advanced by one plane per iteration
+  const int64_t nxy = (int64_t)L.nx * L.ny;
+  int64_t o = (int64_t(kb) * L.ny + j) * L.nx + i;  // table index of the own point
+  double* const t_d1 = tab + (int64_t)(3 * max(e1, 0)) * ni;
+  double* const t_dd = tab + (int64_t)(45 + 6 * max(e2, 0)) * ni;
+  double* const t_adv = tab + (int64_t)(111 + gf) * ni;
+  const double* bb = in + V_BETA * L.gfs + L.idx(i, j, kb);
   for (int k = kb; k < ke; ++k) {
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // plane k + 3 has landed (k + 4 may not)
     __syncthreads();  // ... for every thread, and plane k - 3's slot is no longer read
@@ -927,15 +934,13 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
         return 8.0 * (F(ox + sx, oy + sy_, oz + sz) - F(ox - sx, oy - sy_, oz - sz)) -
                (F(ox + 2 * sx, oy + 2 * sy_, oz + 2 * sz) - F(ox - 2 * sx, oy - 2 * sy_, oz - 2 * sz));
       };
-      const int64_t o = (int64_t(k) * L.ny + j) * L.nx + i;
-      const int64_t cg = L.idx(i, j, k);
       const double f0 = F(0, 0, 0);
       if (e1 >= 0) {
 #pragma unroll
-        for (int l = 0; l < 3; ++l) __stcs(tab + (3 * e1 + l) * ni + o, D1(l, 0, 0, 0) * K.i12h[l]);
+        for (int l = 0; l < 3; ++l) __stcs(t_d1 + l * ni + o, D1(l, 0, 0, 0) * K.i12h[l]);
       }
       if (e2 >= 0) {
-        double* tt = tab + (45 + 6 * e2) * ni + o;
+        double* tt = t_dd + o;
 #pragma unroll
         for (int p = 0; p < 6; ++p) {
           const int l = sI(p), m = sJ(p);
@@ -958,7 +963,7 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int sx = q == 0, sy_ = q == 1, sz = q == 2;
-        const double beta = ld(in + (V_BETA + q) * L.gfs + cg);
+        const double beta = ld(bb + q * L.gfs);
         const double a1 = F(sx, sy_, sz), b1 = F(-sx, -sy_, -sz);
         const double a2 = F(2 * sx, 2 * sy_, 2 * sz), b2 = F(-2 * sx, -2 * sy_, -2 * sz);
         const double a3 = F(3 * sx, 3 * sy_, 3 * sz), b3 = F(-3 * sx, -3 * sy_, -3 * sz);
@@ -966,10 +971,12 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
         const double A = 15.0 * (a1 + b1) - 6.0 * (a2 + b2) + (a3 + b3) - 20.0 * f0;
         r = fma(fma(beta, S, fabs(beta) * A), K.i24h[q], r);
       }
-      __stcs(tab + (111 + gf) * ni + o, r);
+      __stcs(t_adv + o, r);
     }
 #pragma unroll
     for (int q = 0; q < 2 * DR; ++q) zq[q] = zq[q + 1];
+    o += nxy;
+    bb += L.plane;
   }
 }
 
