@@ -824,10 +824,10 @@ constexpr int NTAB = NSLOT - T_D1;            // 136
 // differentiated, the 6 second derivatives if twice differentiated, the advection term)
 // with streaming stores.  Same operation order as StencilP (D1raw, D2raw, D11raw, ADVraw).
 constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 * DR, DPL = DSX * DSY;
-constexpr int DZC = 48, DRING = 8, DNT = DT_X * DT_Y;
+constexpr int DZC = 32, DRING = 8, DNT = DT_X * DT_Y;
 
 template <int STAGE>
-__global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty) {
+__global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty, int dzc) {
   extern __shared__ __align__(16) double dring[];
   double (*ring)[DPL] = reinterpret_cast<double (*)[DPL]>(dring);
   double* gzb = dring + DRING * DPL;   // D1raw_z f on the whole plane (tile + halo)
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int
   const int t = blockIdx.y;
   const int bx = t % ntx, by = (t / ntx) % nty, ch = t / (ntx * nty);
   const int i0 = bx * DT_X, j0 = by * DT_Y;
-  const int kb = a.k_begin + ch * DZC, ke = min(kb + DZC, a.k_end);
+  const int kb = a.k_begin + ch * dzc, ke = min(kb + dzc, a.k_end);
   const double* in = stage_input<STAGE>(a);
   const double* f = in + gf * L.gfs;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1021,11 +1021,17 @@ cudaError_t launch_hbm(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
   const unsigned gx = (unsigned)((a.L.nx + 31) / 32), gy = (unsigned)((a.L.ny + 3) / 4);
   {
     const int ntx = (int)((a.L.nx + DT_X - 1) / DT_X), nty = (int)((a.L.ny + DT_Y - 1) / DT_Y);
-    const int nch = (nk + DZC - 1) / DZC;
+    static int dzc = 0;  // z planes per CTA (CHEMORA_BSSN_DZC, default DZC)
+    if (!dzc) {
+      const char* e = getenv("CHEMORA_BSSN_DZC");
+      dzc = e ? atoi(e) : DZC;
+      if (dzc < 1) dzc = DZC;
+    }
+    const int nch = (nk + dzc - 1) / dzc;
     constexpr int smem = (DRING * DPL + DPL + DT_Y * DSX) * 8;
     static std::atomic<uint64_t> attr_done{0};
     if (cudaError_t e = smem_optin((const void*)bssn_deriv<STAGE>, smem, attr_done); e != cudaSuccess) return e;
-    bssn_deriv<STAGE><<<dim3(NV, (unsigned)(ntx * nty * nch), 1), DNT, smem, st>>>(a, K, ntx, nty);
+    bssn_deriv<STAGE><<<dim3(NV, (unsigned)(ntx * nty * nch), 1), DNT, smem, st>>>(a, K, ntx, nty, dzc);
   }
   // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM for the algebra kernels (register cap)
   static int mb = -1;
