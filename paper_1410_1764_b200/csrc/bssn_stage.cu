@@ -22,6 +22,7 @@
 // A = (D+ - D-)/2 (identical to max(beta,0) D+ + min(beta,0) D-).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include "grid.hpp"
@@ -1033,30 +1034,27 @@ cudaError_t launch_hbm(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
     if (cudaError_t e = smem_optin((const void*)bssn_deriv<STAGE>, smem, attr_done); e != cudaSuccess) return e;
     bssn_deriv<STAGE><<<dim3(NV, (unsigned)(ntx * nty * nch), 1), DNT, smem, st>>>(a, K, ntx, nty, dzc);
   }
-  // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM for the algebra kernels (register cap)
-  static int mb = -1;
-  if (mb < 0) {
+  // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM of the algebra kernels (register cap),
+  // one digit for both groups or two digits (G2, G13)
+  static int mb2 = -1, mb13 = -1;
+  if (mb2 < 0) {
     const char* e = getenv("CHEMORA_BSSN_ALG_MB");
-    mb = e ? atoi(e) : 3;
+    const int v = e ? atoi(e) : 2;
+    mb2 = v >= 10 ? v / 10 : v;
+    mb13 = v >= 10 ? v % 10 : v;
   }
   const dim3 grid(gx, gy, (unsigned)nk);
-  switch (mb) {
-    case 2:
-      bssn_alg<STAGE, 2, 2><<<grid, block, 0, st>>>(a, K, dst);
-      bssn_alg<STAGE, 13, 2><<<grid, block, 0, st>>>(a, K, dst);
-      break;
-    case 3:
-      bssn_alg<STAGE, 2, 3><<<grid, block, 0, st>>>(a, K, dst);
-      bssn_alg<STAGE, 13, 3><<<grid, block, 0, st>>>(a, K, dst);
-      break;
-    case 4:
-      bssn_alg<STAGE, 2, 4><<<grid, block, 0, st>>>(a, K, dst);
-      bssn_alg<STAGE, 13, 4><<<grid, block, 0, st>>>(a, K, dst);
-      break;
-    default:
-      bssn_alg<STAGE, 2, 1><<<grid, block, 0, st>>>(a, K, dst);
-      bssn_alg<STAGE, 13, 1><<<grid, block, 0, st>>>(a, K, dst);
-  }
+  auto run = [&](auto g, int mb) {
+    constexpr int G = decltype(g)::value;
+    switch (mb) {
+      case 2: bssn_alg<STAGE, G, 2><<<grid, block, 0, st>>>(a, K, dst); break;
+      case 3: bssn_alg<STAGE, G, 3><<<grid, block, 0, st>>>(a, K, dst); break;
+      case 4: bssn_alg<STAGE, G, 4><<<grid, block, 0, st>>>(a, K, dst); break;
+      default: bssn_alg<STAGE, G, 1><<<grid, block, 0, st>>>(a, K, dst);
+    }
+  };
+  run(std::integral_constant<int, 2>{}, mb2);
+  run(std::integral_constant<int, 13>{}, mb13);
   return cudaGetLastError();
 }
 
