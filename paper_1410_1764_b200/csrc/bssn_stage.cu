@@ -828,7 +828,7 @@ constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 *
 constexpr int DZC = 32, DRING = 8, DNT = DT_X * DT_Y;
 
 template <int STAGE>
-__global__ void __launch_bounds__(DNT, 4) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty, int dzc) {
+__global__ void __launch_bounds__(DNT, 1024 / DNT) bssn_deriv(StageLaunch a, BssnK K, int ntx, int nty, int dzc) {
   extern __shared__ __align__(16) double dring[];
   double (*ring)[DPL] = reinterpret_cast<double (*)[DPL]>(dring);
   double* gzb = dring + DRING * DPL;   // D1raw_z f on the whole plane (tile + halo)
