@@ -166,6 +166,9 @@ def oracle_sample(system: str, seconds_target: float = 15.0):
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
+    # rank 0 runs the oracle alone (the other ranks exit), so it gets the host's cores even
+    # under torchrun, which defaults OMP_NUM_THREADS to 1 (read when liboracle loads)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     cfg = workload(args)
     per = max(2.0, 20.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
