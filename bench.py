@@ -4,7 +4,8 @@
 
 Default workload (N=1): configs[1], the scalar wave equation Eq. 1,
 4th-order FD, 512^3 fp64, periodic, 3 ghosts, fused RHS + RK4 update.  A step is one
-classical RK4 step of the whole grid = the 4 fused stage kernels.  Inputs (23 GB of state)
+classical RK4 step of the whole grid: for the wave by default two temporally blocked kernels
+(stages 1+2, 3+4), for BSSN a derivative + two algebra kernels per stage.  Inputs (23 GB of state)
 are larger than the 126 MB L2, so no explicit flush is needed between steps.
 
 Multi-GPU (torchrun, one process per GPU): z-slab decomposition, 512^3 per GPU (weak
@@ -338,16 +339,24 @@ def main():
         # on one GPU up to three grid handles take turns on their own streams, so one
         # handle's upload, another's step and a third's download overlap (H2D engine, SMs,
         # D2H engine); each step still moves its whole input and output over PCIe
+        # pinned host buffers: 2 per handle per rank on this node, kept under half the RAM
+        import psutil
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        max_nb = int(0.5 * psutil.virtual_memory().available // (2 * nbytes * local_world))
         grids = [g]
-        while world == 1 and len(grids) < 3 and torch.cuda.mem_get_info()[0] > g.nbytes + (2 << 30):
+        while (world == 1 and len(grids) < min(3, max_nb)
+               and torch.cuda.mem_get_info()[0] > g.nbytes + (2 << 30)):
             g2 = P.Grid(system, gext, h, device=local, rank=rank, nranks=world)
             if args.variant is not None:
                 g2.set_kernel_variant(args.variant)
             grids.append(g2)
         nb = len(grids)
         pipelined = nb > 1
-        host_in = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(nb)]
-        host_out = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(nb)]
+        if max_nb < 1:
+            raise SystemExit(f"e2e: {2 * nbytes * local_world / 2**30:.0f} GiB of pinned host buffers "
+                             f"do not fit this node's RAM; rerun with --e2e-steps 0")
+        host_in = [torch.empty(shape, dtype=torch.float64, pin_memory=True) for _ in range(nb)]
+        host_out = [torch.empty(shape, dtype=torch.float64, pin_memory=True) for _ in range(nb)]
         g.get_state(out=host_in[0].numpy())
         for t in host_in[1:]:
             t.copy_(host_in[0])
