@@ -231,6 +231,8 @@ def main():
     # amortised -- per step the two PCIe directions then overlap (scripts/pcie_probe.py)
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--variant", type=int, default=None, help="stage-kernel variant (testing)")
+    ap.add_argument("--fd-order", type=int, default=4, choices=[2, 4, 6, 8],
+                    help="wave: accuracy order of the centered stencils (NEXT-1, PAPER.md:512-514)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -258,7 +260,11 @@ def main():
     L = 2 * math.pi if system == C.SYS_WAVE else 1.0
     h = (L / n[0], L / n[1], L / n[2])
     dt = 0.25 * min(h)
-    g = P.Grid(system, gext, h, device=local, rank=rank, nranks=world)
+    order = args.fd_order if system == C.SYS_WAVE else 4
+    ghost = max(3, order // 2)
+    if order != 4:
+        cfg["config"] = dict(cfg["config"], fd_order=order, ghost=ghost)
+    g = P.Grid(system, gext, h, device=local, rank=rank, nranks=world, ghost=ghost, fd_order=order)
     if args.variant is not None:
         g.set_kernel_variant(args.variant)
     if world > 1:
@@ -303,7 +309,7 @@ def main():
     pair_kernels = cfg["system"] == "wave" and variant in (6, 7, 8)   # temporally blocked pairs
     bpp = 256 if pair_kernels else floor_bpp
     achieved = bpp * pts_local / mean_step_s / 1e9
-    traffic = measured_traffic(args.config, variant)
+    traffic = measured_traffic(args.config, variant) if order == 4 else None
     kname = ({6: "wave_fused<A>, wave_fused<B>", 7: "wave_fused2<A>, wave_fused2<B>",
               8: "wave_fused3<A>, wave_fused3<B>"}.get(variant, "") + " (2 launches = 1 step)" if bpp == 256 else
              "stage kernels (4 launches x groups = 1 step)")
@@ -346,7 +352,7 @@ def main():
         grids = [g]
         while (world == 1 and len(grids) < min(3, max_nb)
                and torch.cuda.mem_get_info()[0] > g.nbytes + (2 << 30)):
-            g2 = P.Grid(system, gext, h, device=local, rank=rank, nranks=world)
+            g2 = P.Grid(system, gext, h, device=local, rank=rank, nranks=world, ghost=ghost, fd_order=order)
             if args.variant is not None:
                 g2.set_kernel_variant(args.variant)
             grids.append(g2)
