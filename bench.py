@@ -247,8 +247,17 @@ def main():
     from paper_1410_1764_b200 import capi as C
 
     torch.cuda.set_device(local)
+    watchdog = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # the multi-rank step orders its phases with stream waits on neighbour flags; if a
+        # peer never signals, fail the run instead of hanging it (CHEMORA_BENCH_DEADLINE s)
+        def _abort():
+            print(f"rank {rank}: bench exceeded CHEMORA_BENCH_DEADLINE, aborting", file=sys.stderr, flush=True)
+            os._exit(3)
+        watchdog = threading.Timer(float(os.environ.get("CHEMORA_BENCH_DEADLINE", "900")), _abort)
+        watchdog.daemon = True
+        watchdog.start()
     cfg = workload(args)
     n = cfg["n"]
     system = C.SYS_WAVE if cfg["system"] == "wave" else C.SYS_BSSN
@@ -410,6 +419,7 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        watchdog.cancel()
         dist.destroy_process_group()
     return 0
 
