@@ -241,10 +241,11 @@ int chemora_autotune(chemora_grid_t grid, int32_t trials, int32_t* chosen, doubl
 /* ---- testing hooks (not part of the user-facing contract) */
 
 /* Select the kernel design of this handle.  WAVE: 0 = one thread per point,
- * 1 = same in plain order, 2 = register z-march, 3/4 = TMA z-marches, 5 = SMEM brick (one
- * kernel per RK stage), 6 = temporally blocked stage pairs on 32x8 tiles, 7 = the same on
- * 32x16 tiles, 8 = 6 with register-queue z stencils (default for 4th order); every wave
- * design is bitwise identical.  BSSN: 0 =
+ * 1 = same in plain order, 2 = register z-march, 3/4 = TMA z-marches (4: every order; the
+ * default for orders 6/8 when the 32x16 tiles fill the SMs), 5 = SMEM brick (one kernel per
+ * RK stage), 6 = temporally blocked stage pairs on 32x8 tiles, 7 = the same on 32x16 tiles,
+ * 8 = 6 with register-queue z stencils (default for 4th order; 6-8 are 4th order only);
+ * every wave design is bitwise identical.  BSSN: 0 =
  * two-phase SMEM table, 1 = fused single kernel, 2 = fissioned G1/G2/G3, 3 = HBM derivative
  * table + algebra kernels (default); results agree to rounding. */
 int chemora_set_kernel_variant(chemora_grid_t grid, int variant);

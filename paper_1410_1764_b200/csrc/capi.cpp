@@ -432,11 +432,17 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->ipc = false;
   g->cur = 0;
   // default tiling: the temporally blocked stage pairs with register-queue z stencils for
-  // 4th-order wave grids (variant 8, fastest measured, profiles/r1_wave_design_study.md),
-  // else one thread per point; BSSN: fission
-  // at the derivative/algebra boundary through the HBM table (fastest measured at 192^3)
-  g->variant = desc->system == CHEMORA_SYS_BSSN ? 3 /* HBM derivative table */
-             : (desc->fd_order == 0 || desc->fd_order == 4) ? kVariantFused3 : 0;
+  // 4th-order wave grids (variant 8, fastest measured, profiles/r1_wave_design_study.md);
+  // orders 6/8: the persistent TMA z-march when its 32x16 tiles fill the SMs (variant 4:
+  // 14.2 vs 15.6-18.1 ms/step at 512^3, profiles/r1_fd_orders.jsonl), else one thread per
+  // point (also for order 2, where it is fastest); BSSN: fission at the derivative/algebra
+  // boundary through the HBM table (fastest measured at 192^3)
+  {
+    const int order = desc->fd_order == 0 ? 4 : desc->fd_order;
+    const int64_t tiles16 = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
+    g->variant = desc->system == CHEMORA_SYS_BSSN ? 3 /* HBM derivative table */
+               : order == 4 ? kVariantFused3 : (order >= 6 && tiles16 >= 148) ? 4 : 0;
+  }
   const char* v = getenv("CHEMORA_KERNEL_VARIANT");
   if (v) g->variant = atoi(v);
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
@@ -704,7 +710,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     cands.push_back({0, 0});
     const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
-    if (order <= 4 && tiles >= 148) cands.push_back({4, 0});
+    if (tiles >= 148) cands.push_back({4, 0});
     if (order == 4 && g->L.g >= 4) {
       cands.push_back({kVariantFused, 0});
       cands.push_back({kVariantFused3, 0});

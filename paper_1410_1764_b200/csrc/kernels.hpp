@@ -51,7 +51,7 @@ cudaError_t wave_fused_pair(const StageLaunch& a, int pair, cudaStream_t st);
 cudaError_t wave_fused2_pair(const StageLaunch& a, int pair, cudaStream_t st);
 // variant 8 (wave_fused3.cu): the pairs with own-column z stencils from register queues
 cudaError_t wave_fused3_pair(const StageLaunch& a, int pair, cudaStream_t st);
-// persistent TMA z-march (wave_tma.cu), fd_order 2 or 4, stages 1..4
+// persistent TMA z-march (wave_tma.cu), fd_order 2/4/6/8, stages 1..4
 cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st);
 
 // BSSN (App. A) ------------------------------------------------------------------------

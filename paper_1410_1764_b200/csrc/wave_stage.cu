@@ -625,7 +625,7 @@ cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStr
   // 2: register-queue z-march; 3: TMA z-march (W <= 2).  RHS-only uses the simple kernel.
   // the fused energy monitor (NEXT-3) lives in the one-thread-per-point stage-4 kernel
   const bool mon = stage == 4 && a.mon_partials != nullptr;
-  if (a.variant == 4 && W <= 2 && stage >= 1 && !mon) return wave_tma_stage(a, stage, st);
+  if (a.variant == 4 && stage >= 1 && !mon) return wave_tma_stage(a, stage, st);
   if (a.variant == 5 && !mon) {
     switch (stage) {
       case 1: return launch_brick<1, W>(a, K, st);

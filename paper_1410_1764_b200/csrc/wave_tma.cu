@@ -45,13 +45,15 @@ struct Cfg {
   // 16-byte boundary in x (an odd fp64 offset raises an illegal-instruction fault)
   static constexpr int H = (W + 1) / 2 * 2;
   static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
-  static constexpr int RZ = 2 * W + 3, RP = 3;
+  static constexpr int RZ = 2 * W + 3;
   static constexpr int C = TX * TY;  // points per tile plane
   static constexpr int ZRHO_B = r128(RX * RY * 8), ZV3_B = r128(C * 8), ZSLOT = ZRHO_B + ZV3_B;
   static constexpr int PV1_B = r128(RX * TY * 8), PV2_B = r128(TX * RY * 8);
   static constexpr int PY_B = r128(PW<STAGE>::NY * C * 8), PQ_B = r128(PW<STAGE>::NQ * C * 8),
                        PU_B = r128(PW<STAGE>::NU * C * 8);
   static constexpr int PSLOT = PV1_B + PV2_B + PY_B + PQ_B + PU_B;
+  // three pointwise slots, or two where the radius-4 z ring leaves no room (stage 4, W = 4)
+  static constexpr int RP = RZ * ZSLOT + 3 * PSLOT + (2 * RZ + 6) * 8 <= 227 * 1024 ? 3 : 2;
   static constexpr uint32_t ZBYTES = (RX * RY + C) * 8;
   static constexpr uint32_t PBYTES = (RX * TY + TX * RY + (PW<STAGE>::NY + PW<STAGE>::NQ + PW<STAGE>::NU) * C) * 8;
   static constexpr int SMEM = RZ * ZSLOT + RP * PSLOT + (2 * RZ + 2 * RP) * 8;
@@ -313,6 +315,8 @@ cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st) {
   switch (a.fd_order) {
     case 2: return dispatch<1>(a, stage, st);
     case 4: return dispatch<2>(a, stage, st);
+    case 6: return dispatch<3>(a, stage, st);
+    case 8: return dispatch<4>(a, stage, st);
   }
   return cudaErrorInvalidValue;
 }
