@@ -700,9 +700,9 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
   cudaStream_t st = as_stream(stream);
   // candidate tilings (variant, band), pruned by a footprint model:
   //   wave: one thread per point in plain order (L1/L2 reuse of every stencil operand),
-  //         the persistent TMA z-march (only when its 32x16 tiles fill the SMs and the
-  //         stencil radius is <= 2), and for 4th order the two temporally blocked pair
-  //         kernels (32x8 and 32x16 tiles), else the banded L2-window order;
+  //         the persistent TMA z-march (only when its 32x16 tiles fill the SMs), and for
+  //         4th order the two temporally blocked pair kernels (32x8 tiles: variants 6 and
+  //         8), else the banded L2-window order;
   //   BSSN: fissioned kernels, and the fused single kernel only for small grids (it spills).
   struct Cand { int variant, band; };
   std::vector<Cand> cands;

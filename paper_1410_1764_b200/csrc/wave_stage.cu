@@ -622,7 +622,8 @@ template <int W>
 cudaError_t dispatch_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
   const WaveK K = make_k(a);
   // variant 0 (default) and 1: one thread per point (0: banded CTA order, 1: plain order);
-  // 2: register-queue z-march; 3: TMA z-march (W <= 2).  RHS-only uses the simple kernel.
+  // 2: register-queue z-march; 3: TMA z-march (W = 2); 4: persistent TMA z-march (any W,
+  // wave_tma.cu).  RHS-only uses the simple kernel.
   // the fused energy monitor (NEXT-3) lives in the one-thread-per-point stage-4 kernel
   const bool mon = stage == 4 && a.mon_partials != nullptr;
   if (a.variant == 4 && stage >= 1 && !mon) return wave_tma_stage(a, stage, st);
