@@ -181,6 +181,35 @@ def test_kernel_variants_bitwise_identical():
         assert np.array_equal(out[0], o), f"variant {v} differs"
 
 
+@pytest.mark.parametrize("order", [2, 6, 8])
+def test_wide_stencil_tilings_bitwise_identical(order):
+    """NEXT-1 orders through every tiling that takes them (one thread per point, plain
+    order, register z-march, persistent TMA z-march with radius-3/4 boxes), on one grid and
+    on two z-slabs: bitwise identical states."""
+    P, C = _mods()
+    n = (70, 45, 40)
+    h = tuple(2 * math.pi / v for v in n)
+    gh = max(3, order // 2)
+    y0 = ci.noise(n, 5, seed=order)
+    dt = 0.2 * min(h)
+    out = []
+    variants = (0, 1, 2, 4)
+    for v in variants:
+        g = P.Grid(C.SYS_WAVE, n, h, ghost=gh, fd_order=order)
+        g.set_kernel_variant(v)
+        g.set_initial(C.INIT_HOST, y0)
+        g.rk4_step(dt, 3)
+        out.append(g.get_state())
+    for v, o in zip(variants[1:], out[1:]):
+        assert np.array_equal(out[0], o), f"order {order}: variant {v} differs"
+    s = P.LocalSlabs(C.SYS_WAVE, n, h, 2, ghost=gh, fd_order=order)
+    for gg in s.grids:
+        gg.set_kernel_variant(4)
+    s.set_initial(C.INIT_HOST, y0)
+    s.rk4_step(dt, 3)
+    assert np.array_equal(s.get_state(), out[0])
+
+
 def _box_oracle_one_step(gext, h, dt, seed, center, R=10):
     """Oracle value at ``center`` after ONE RK4 step of the NOISE data of a periodic grid
     of extents ``gext``: the oracle runs periodically on a (2R+1)^3 box; wrap errors
