@@ -819,11 +819,15 @@ __global__ void __launch_bounds__(64) bssn_tab(StageLaunch a, BssnK K, double* r
 // the register-heavy algebra has no stencil loads in flight.  Table traffic: 136 x 8 B
 // written + read per point per stage.
 constexpr int NTAB = NSLOT - T_D1;            // 136
-// Derivative kernel: one CTA per (32 x 8 tile, z chunk, GF).  It marches the chunk with an
-// 8-plane shared-memory ring of the GF's planes (tile + 3-point halo), so every stencil
-// operand is read from HBM/L2 once per CTA, and writes all table slots of that GF (D1 if
-// differentiated, the 6 second derivatives if twice differentiated, the advection term)
-// with streaming stores.  Same operation order as StencilP (D1raw, D2raw, D11raw, ADVraw).
+// Derivative kernel: one CTA per (32 x 8 tile, z chunk of DZC planes, GF), 4 CTAs per SM.
+// It marches the chunk with an 8-plane shared-memory ring of the GF's planes (tile + 3-point
+// halo; cp.async, two planes in flight), so every stencil operand is read from HBM/L2 once
+// per CTA; the own column's z stencils come from a register queue, the own x row and y
+// column are read from the ring once per plane, and the inner derivatives of the mixed
+// second derivatives are computed once per plane for the whole tile.  It writes all table
+// slots of that GF (D1 if differentiated, the 6 second derivatives if twice differentiated,
+// the advection term) with streaming stores.  Same operation order as StencilP (D1raw,
+// D2raw, D11raw, ADVraw).  Design steps and probes: profiles/r1_bssn_summary.md.
 constexpr int DT_X = 32, DT_Y = 8, DR = 3, DSX = DT_X + 2 * DR, DSY = DT_Y + 2 * DR, DPL = DSX * DSY;
 constexpr int DZC = 32, DRING = 8, DNT = DT_X * DT_Y;
 
@@ -846,8 +850,8 @@ __global__ void __launch_bounds__(DNT, 1024 / DNT) bssn_deriv(StageLaunch a, Bss
   const bool live = i < L.nx && j < L.ny;
   const int64_t ni = L.nx * L.ny * L.nz;
   const int xmax = (int)L.nx + L.g - 1, ymax = (int)L.ny + L.g - 1;
-  // asynchronous plane copies (cp.async, one commit group per plane): the copy of plane
-  // k + 4 overlaps the computation of plane k
+  // asynchronous plane copies (cp.async, one commit group per plane): the copies of planes
+  // k + 4 and k + 5 overlap the computation of plane k
   // this thread's elements of a ring plane are the same for every plane: their in-plane
   // offsets are computed once (the plane loop then only adds the plane base)
   constexpr int NE = (DPL + DNT - 1) / DNT;
