@@ -1026,39 +1026,18 @@ cudaError_t launch_hbm(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
   const unsigned gx = (unsigned)((a.L.nx + 31) / 32), gy = (unsigned)((a.L.ny + 3) / 4);
   {
     const int ntx = (int)((a.L.nx + DT_X - 1) / DT_X), nty = (int)((a.L.ny + DT_Y - 1) / DT_Y);
-    static int dzc = 0;  // z planes per CTA (CHEMORA_BSSN_DZC, default DZC)
-    if (!dzc) {
-      const char* e = getenv("CHEMORA_BSSN_DZC");
-      dzc = e ? atoi(e) : DZC;
-      if (dzc < 1) dzc = DZC;
-    }
+    constexpr int dzc = DZC;  // z planes per CTA (profiles/r1_bssn_summary.md: 32 measured best)
     const int nch = (nk + dzc - 1) / dzc;
     constexpr int smem = (DRING * DPL + DPL + DT_Y * DSX) * 8;
     static std::atomic<uint64_t> attr_done{0};
     if (cudaError_t e = smem_optin((const void*)bssn_deriv<STAGE>, smem, attr_done); e != cudaSuccess) return e;
     bssn_deriv<STAGE><<<dim3(NV, (unsigned)(ntx * nty * nch), 1), DNT, smem, st>>>(a, K, ntx, nty, dzc);
   }
-  // CHEMORA_BSSN_ALG_MB: minimum resident CTAs per SM of the algebra kernels (register cap),
-  // one digit for both groups or two digits (G2, G13)
-  static int mb2 = -1, mb13 = -1;
-  if (mb2 < 0) {
-    const char* e = getenv("CHEMORA_BSSN_ALG_MB");
-    const int v = e ? atoi(e) : 2;
-    mb2 = v >= 10 ? v / 10 : v;
-    mb13 = v >= 10 ? v % 10 : v;
-  }
+  // algebra kernels at 2 resident CTAs per SM (up to 255 registers, spill-free: measured
+  // best against 3 and 4 CTAs/SM, profiles/r1_bssn_summary.md)
   const dim3 grid(gx, gy, (unsigned)nk);
-  auto run = [&](auto g, int mb) {
-    constexpr int G = decltype(g)::value;
-    switch (mb) {
-      case 2: bssn_alg<STAGE, G, 2><<<grid, block, 0, st>>>(a, K, dst); break;
-      case 3: bssn_alg<STAGE, G, 3><<<grid, block, 0, st>>>(a, K, dst); break;
-      case 4: bssn_alg<STAGE, G, 4><<<grid, block, 0, st>>>(a, K, dst); break;
-      default: bssn_alg<STAGE, G, 1><<<grid, block, 0, st>>>(a, K, dst);
-    }
-  };
-  run(std::integral_constant<int, 2>{}, mb2);
-  run(std::integral_constant<int, 13>{}, mb13);
+  bssn_alg<STAGE, 2, 2><<<grid, block, 0, st>>>(a, K, dst);
+  bssn_alg<STAGE, 13, 2><<<grid, block, 0, st>>>(a, K, dst);
   return cudaGetLastError();
 }
 
@@ -1066,15 +1045,7 @@ template <int STAGE, int G>
 cudaError_t launch(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
-  // CTA shape (128 threads): CHEMORA_BSSN_BLOCK = "BXxBYxBZ" (default 32x4x1).
-  static int bdim[3] = {0, 0, 0};
-  if (!bdim[0]) {
-    bdim[0] = 32; bdim[1] = 4; bdim[2] = 1;
-    if (const char* e = getenv("CHEMORA_BSSN_BLOCK")) {
-      int x, y, z;
-      if (sscanf(e, "%dx%dx%d", &x, &y, &z) == 3 && x * y * z == 128) { bdim[0] = x; bdim[1] = y; bdim[2] = z; }
-    }
-  }
+  constexpr int bdim[3] = {32, 4, 1};  // CTA shape (128 threads)
   dim3 block(bdim[0], bdim[1], bdim[2]);
   dim3 grid((unsigned)((a.L.nx + bdim[0] - 1) / bdim[0]), (unsigned)((a.L.ny + bdim[1] - 1) / bdim[1]),
             (unsigned)((nk + bdim[2] - 1) / bdim[2]));
@@ -1093,9 +1064,10 @@ cudaError_t launch_tab(const StageLaunch& a, const BssnK& K, double* dst, cudaSt
 
 template <int STAGE>
 cudaError_t launch_stage(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
-  // variant 0: two-phase SMEM table kernel; 1: fused single kernel (stencils from global
-  // memory); 2: the fissioned kernels G1, G2, G3; 3: HBM derivative table + algebra kernels
-  if (a.variant == 1) return launch<STAGE, 0>(a, K, dst, st);
+  // variant 0: two-phase SMEM table kernel; 2: the fissioned kernels G1, G2, G3; 3: HBM
+  // derivative table + algebra kernels.  (Variant 1, the fused single kernel, spilled 33 KB
+  // per thread and ran 8x slower -- the NEXT-2 fission result, profiles/r1_bssn_summary.md --
+  // and is gone.)
   if (a.variant == 3) return launch_hbm<STAGE>(a, K, dst, st);
   if (a.variant == 2) {
     cudaError_t e = launch<STAGE, 1>(a, K, dst, st);

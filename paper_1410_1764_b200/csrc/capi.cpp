@@ -174,7 +174,7 @@ WsPlan plan_ws(const Layout& L, int system) {
 }
 
 Layout layout_of(const chemora_grid_desc& d) {
-  // storage ghost width: the temporally blocked wave kernels (wave_fused.cu) read their
+  // storage ghost width: the temporally blocked wave kernels (wave_fused3.cu) read their
   // inputs with a halo of two stacked 4th-order stencils, so 4th-order wave grids keep at
   // least 4 ghost layers in HBM; the API's ghost width (desc.ghost) is unchanged.
   int gs = d.ghost;
@@ -302,21 +302,18 @@ cudaError_t launch_stage(chemora_grid_t g, const StageLaunch& a, int stage, cuda
   return g->desc.system == CHEMORA_SYS_WAVE ? wave_stage(a, stage, st) : bssn_stage(a, stage, st);
 }
 
-// Temporally blocked wave step (wave_fused.cu): two kernels per step, the new state lands
-// in the scratch set, which then becomes the state set.
-// Variant 6: 32x8 tiles (wave_fused.cu); variant 7: 32x16 tiles, two rows per thread
-// (wave_fused2.cu).
-constexpr int kVariantFused = 6, kVariantFused2 = 7, kVariantFused3 = 8;
-bool is_fused_variant(int v) { return v == kVariantFused || v == kVariantFused2 || v == kVariantFused3; }
+// Temporally blocked wave step (wave_fused3.cu, variant 8): two kernels per step, the new
+// state lands in the scratch set, which then becomes the state set.  (The round-1 pair
+// designs 6 and 7 were slower in every measured configuration and are gone.)
+constexpr int kVariantFused3 = 8;
+bool is_fused_variant(int v) { return v == kVariantFused3; }
 bool use_fused(chemora_grid_t g) {
   const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
-  // the energy monitor is fused into kernel B of variants 6 and 8 (not 7)
-  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 &&
-         !(g->monitor && g->variant == kVariantFused2) && g->L.g >= 4;
+  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 && g->L.g >= 4;
 }
 cudaError_t fused_pair(int variant, const StageLaunch& a, int pair, cudaStream_t st) {
-  if (variant == kVariantFused3) return wave_fused3_pair(a, pair, st);
-  return variant == kVariantFused2 ? wave_fused2_pair(a, pair, st) : wave_fused_pair(a, pair, st);
+  (void)variant;
+  return wave_fused3_pair(a, pair, st);
 }
 void swap_state(chemora_grid_t g) {
   std::swap(g->sets.y, g->sets.b);
@@ -443,13 +440,9 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
     g->variant = desc->system == CHEMORA_SYS_BSSN ? 3 /* HBM derivative table */
                : order == 4 ? kVariantFused3 : (order >= 6 && tiles16 >= 148) ? 4 : 0;
   }
-  const char* v = getenv("CHEMORA_KERNEL_VARIANT");
-  if (v) g->variant = atoi(v);
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
-  // slower under the power cap (profiles/r1_wave_summary.md); -1 = auto band
+  // slower under the power cap (profiles/r1_wave_summary.md); autotune may pick it (-1)
   g->band = 0;
-  const char* bnd = getenv("CHEMORA_WAVE_BAND");
-  if (bnd) g->band = atoi(bnd);
   unsigned long long init[3] = {~0ull, 0ull, 0ull};
   cudaError_t e = cudaMemcpy(g->dparams, g->params, sizeof(g->params), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(fl, init, sizeof(init), cudaMemcpyHostToDevice);
@@ -487,6 +480,10 @@ int chemora_get_kernel_variant(chemora_grid_t g, int* variant) {
 
 int chemora_set_kernel_variant(chemora_grid_t g, int variant) {
   if (int rc = check_grid(g)) return rc;
+  const bool ok = g->desc.system == CHEMORA_SYS_WAVE ? (variant >= 0 && variant <= 5) || variant == kVariantFused3
+                                                    : (variant == 0 || variant == 2 || variant == 3);
+  if (!ok) return fail(CHEMORA_E_INVALID, "unknown kernel variant " + std::to_string(variant));
+  if (g->ipc) return fail(CHEMORA_E_PEER, "the kernel design of a peer-connected slab is fixed at connect time");
   g->variant = variant;
   return CHEMORA_OK;
 }
@@ -645,16 +642,10 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
   cudaStream_t st = as_stream(stream);
   const bool mon = g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0;
   const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
-  static int dbg_stop = -1;  // CHEMORA_DEBUG_STOP=s: run only stages <= s (test hook)
-  if (dbg_stop < 0) {
-    const char* e = getenv("CHEMORA_DEBUG_STOP");
-    dbg_stop = e ? atoi(e) : 4;
-  }
   if (use_fused(g)) {
     for (int n = 0; n < nsteps; ++n) {
       StageLaunch a = stage_args(g, dt);
       for (int pair = 0; pair < 2; ++pair) {
-        if (2 * pair + 2 > dbg_stop) return CHEMORA_OK;
         if (int rc = phase_wait(g, st)) return rc;
         if (pair == 1 && mon) {
           CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
@@ -675,7 +666,6 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
   for (int n = 0; n < nsteps; ++n) {
     StageLaunch a = stage_args(g, dt);
     for (int s = 1; s <= 4; ++s) {
-      if (s > dbg_stop) return CHEMORA_OK;
       if (int rc = phase_wait(g, st)) return rc;
       if (s == 4 && mon) {
         CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
@@ -712,7 +702,6 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     if (tiles >= 148) cands.push_back({4, 0});
     if (order == 4 && g->L.g >= 4) {
-      cands.push_back({kVariantFused, 0});
       cands.push_back({kVariantFused3, 0});
     } else {
       cands.push_back({0, -1});
@@ -721,7 +710,6 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     cands.push_back({0, 0});
     cands.push_back({2, 0});  // fissioned one-thread-per-point kernels
     cands.push_back({3, 0});  // HBM derivative table + algebra kernels
-    if (g->L.nx * g->L.ny * g->L.nz <= (int64_t)64 * 64 * 64) cands.push_back({1, 0});
   }
   const int saved_v = g->variant, saved_b = g->band;
   cudaEvent_t e0, e1, e2;

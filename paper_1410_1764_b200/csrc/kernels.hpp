@@ -44,12 +44,9 @@ struct StageLaunch {
 // Wave (Eq. 1) -------------------------------------------------------------------------
 cudaError_t wave_stage(const StageLaunch& a, int stage, cudaStream_t st);
 cudaError_t wave_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
-// temporally blocked stage pairs (wave_fused.cu): pair 0 = stages 1+2, pair 1 = stages 3+4
-// (new state into the scratch set s.b); fd_order 4, storage ghost >= 4
-cudaError_t wave_fused_pair(const StageLaunch& a, int pair, cudaStream_t st);
-// variant 7 (wave_fused2.cu): the same pairs on 32x16 tiles, two output rows per thread
-cudaError_t wave_fused2_pair(const StageLaunch& a, int pair, cudaStream_t st);
-// variant 8 (wave_fused3.cu): the pairs with own-column z stencils from register queues
+// variant 8 (wave_fused3.cu): temporally blocked stage pairs, pair 0 = stages 1+2, pair 1 =
+// stages 3+4 (new state into the scratch set s.b), own-column z stencils from register
+// queues; fd_order 4, storage ghost >= 4
 cudaError_t wave_fused3_pair(const StageLaunch& a, int pair, cudaStream_t st);
 // persistent TMA z-march (wave_tma.cu), fd_order 2/4/6/8, stages 1..4
 cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st);

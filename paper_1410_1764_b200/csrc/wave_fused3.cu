@@ -1,5 +1,5 @@
 // wave_fused3.cu -- kernel variant 8: the temporally blocked RK4 stage pairs of
-// wave_fused.cu (Eq. 1) with the z stencils of each thread's
+// the round-1 pair kernel (Eq. 1) with the z stencils of each thread's
 // own column taken from register queues (2.5-D z-march inside the temporal blocking).
 //
 // Every consumer thread owns one output point (ti, tj) of the 32x8 tile, and with it the
@@ -486,15 +486,9 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
   if (cudaError_t e = smem_optin((const void*)wave_fused3<B>, G::SMEM, attr_done); e != cudaSuccess) return e;
   const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
-  // z planes per item (CHEMORA_FUSED_CHUNK, default 128 -- measured best of 32..512 at 512^3):
-  // longer chunks recompute fewer halo
-  // planes, shorter ones balance the persistent CTAs better
-  static int zc = 0;
-  if (!zc) {
-    const char* e = getenv("CHEMORA_FUSED_CHUNK");
-    zc = e ? atoi(e) : 128;
-    if (zc < 4) zc = 64;
-  }
+  // z planes per item (128: measured best of 32..512 at 512^3): longer chunks recompute
+  // fewer halo planes, shorter ones balance the persistent CTAs better
+  constexpr int zc = 128;
   int nchunks = (nk + zc - 1) / zc;
   const int want = (8 * nsm + ntx * nty - 1) / (ntx * nty);
   if (nchunks < want) nchunks = want;

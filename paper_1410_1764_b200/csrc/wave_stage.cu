@@ -237,15 +237,9 @@ template <int STAGE, int W>
 cudaError_t launch_simple(const StageLaunch& a, const WaveK& K, double* dst, cudaStream_t st) {
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
-  // CTA shape 32 x BY x BZ (BY * BZ = 8): BZ > 1 keeps z-neighbour planes inside the CTA
-  // (L1 hits instead of L2 requests).  CHEMORA_WAVE_BZ selects BZ (1, 2, 4, 8).
-  static int bz_env = -1;
-  if (bz_env < 0) {
-    const char* e = getenv("CHEMORA_WAVE_BZ");
-    bz_env = e ? atoi(e) : 1;
-    if (bz_env != 1 && bz_env != 2 && bz_env != 4 && bz_env != 8) bz_env = 1;
-  }
-  const int BZ = (STAGE == 0 || a.variant == 1) ? 1 : bz_env, BY = 8 / BZ;
+  // CTA shape 32 x 8 x 1 (32 x 4 x 2 and 32 x 2 x 4, which keep z neighbours inside the
+  // CTA, measured no faster: profiles/r1_wave_design_study.md)
+  const int BZ = 1, BY = 8;
   dim3 block(32, BY, BZ);
   const int ntx = (int)((a.L.nx + 31) / 32), nty = (int)((a.L.ny + BY - 1) / BY);
   const int ntz = (nk + BZ - 1) / BZ;
@@ -693,13 +687,8 @@ bool encode_set_map(CUtensorMap* out, const double* set_base, int64_t px, int64_
   const cuuint32_t box[4] = {bx, by, 1, bg};
   // L2 promotion: interior rows start on 128-byte (not 256-byte) boundaries, so 256-byte
   // promotion would fetch a neighbour tile's half line with every row (measured: up to 2x
-  // DRAM reads).  Default: no promotion; CHEMORA_TMA_PROMO=0..3 selects NONE/64/128/256 B.
-  static int promo_sel = -1;
-  if (promo_sel < 0) {
-    const char* e = getenv("CHEMORA_TMA_PROMO");
-    promo_sel = e ? atoi(e) : 0;
-  }
-  const CUtensorMapL2promotion promo = (CUtensorMapL2promotion)promo_sel;
+  // DRAM reads): no promotion.
+  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(set_base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,

@@ -270,12 +270,7 @@ cudaError_t launch(const StageLaunch& a, const WaveK& K, cudaStream_t st) {
   const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + Cf::TX - 1) / Cf::TX), nty = (int)((L.ny + Cf::TY - 1) / Cf::TY);
   // chunks of ~64 planes, but enough items for >= 8 per SM (load balance of the round robin)
-  static int chunk_env = -1;
-  if (chunk_env < 0) {
-    const char* e = getenv("CHEMORA_TMA_CHUNK");
-    chunk_env = e ? atoi(e) : 0;
-  }
-  const int target = chunk_env > 0 ? chunk_env : 64;
+  const int target = 64;
   int nchunks = (nk + target - 1) / target;
   const int want = (8 * nsm + ntx * nty - 1) / (ntx * nty);
   if (nchunks < want) nchunks = want;

@@ -1,6 +1,6 @@
-"""GPU tests of the temporally blocked wave step (kernel variants 6, wave_fused.cu, 32x8
-tiles, and 7, wave_fused2.cu, 32x16 tiles with two rows per thread): stages 1+2 and 3+4
-each in one kernel with the intermediate state kept in shared memory.  They must give
+"""GPU tests of the temporally blocked wave step (kernel variant 8, wave_fused3.cu, 32x8
+tiles): stages 1+2 and 3+4 each in one kernel with the intermediate state kept in shared
+memory and registers.  They must give
 bit-identical states to the one-kernel-per-stage path and match the oracle."""
 from __future__ import annotations
 
@@ -13,7 +13,7 @@ import chemora_inputs as ci
 import oracle
 
 pytestmark = pytest.mark.gpu
-FUSED_VARIANTS = [6, 7, 8]
+FUSED_VARIANTS = [8]
 
 
 def _mods():
