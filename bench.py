@@ -246,10 +246,20 @@ def main():
     import paper_1410_1764_b200 as P
     from paper_1410_1764_b200 import capi as C
 
+    # ranks sharing a device (fewer GPUs than ranks, e.g. a 1-GPU box): gloo bootstrap and a
+    # host barrier after every phase (chemora_set_phase_barrier) -- no stream then waits on
+    # another process's work; with one GPU per rank: NCCL group, device-side phase ordering
+    ndev = torch.cuda.device_count()
+    shared = world > ndev
+    if shared:
+        local = local % ndev
     torch.cuda.set_device(local)
     watchdog = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # the multi-rank step orders its phases with stream waits on neighbour flags; if a
         # peer never signals, fail the run instead of hanging it (CHEMORA_BENCH_DEADLINE s)
         def _abort():
@@ -277,7 +287,7 @@ def main():
     if args.variant is not None:
         g.set_kernel_variant(args.variant)
     if world > 1:
-        g.connect_ipc()
+        g.connect_ipc(host_barrier=shared)
     init = C.INIT_PLANE_WAVES if system == C.SYS_WAVE else C.INIT_MINK_PERT
     g.set_initial(init, seed=1410)
     stream = torch.cuda.current_stream()
@@ -301,7 +311,7 @@ def main():
     step_ms = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     pts_local = n[0] * n[1] * (n[2] // world if strong else n[2])
@@ -393,7 +403,7 @@ def main():
         barrier()
         e_ms = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([e_ms], device="cuda")
+            t = torch.tensor([e_ms], device="cpu" if shared else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": pts_local * world * args.e2e_steps / (e_ms * 1e-3), "unit": "grid-point updates/s",

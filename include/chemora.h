@@ -168,7 +168,8 @@ int chemora_halo_exchange_multi(chemora_grid_t* grids, int32_t n, void* stream);
 /* Local reduction partials of y over the local interior (SPEC.md:469-477 reduce; Fig. 1
  * "Energy"): out[3v+0] = sum f^2, out[3v+1] = max|f|, out[3v+2] = sum f
  * for v < n_gf, then (WAVE) out[3 n_gf] = sum 1/2 (rho^2 + v.v).  Deterministic order.
- * Synchronises the stream.  Returns CHEMORA_E_NONFINITE as chemora_get_state. */
+ * Synchronises the stream.  Returns CHEMORA_E_NONFINITE as chemora_get_state.  Not
+ * collective (the building block of chemora_norms). */
 int chemora_norms_partial(chemora_grid_t grid, double* host_out, void* stream);
 
 /* Combine per-rank partials (rank-major, nranks x chemora_norms_len doubles) in rank order
@@ -179,10 +180,29 @@ int chemora_norms_combine(const chemora_grid_desc* desc, const double* partials,
 /* Number of doubles chemora_norms / chemora_norms_partial write: 3 n_gf (+1 for WAVE). */
 int chemora_norms_len(int32_t system, int32_t n_gf);
 
-/* nranks == 1 convenience: partial + combine. */
+/* Global norms of y (SPEC.md:469-477 reduce; "Energy"): host_out
+ * (chemora_norms_len doubles) = per GF L2 = sqrt(h^3 sum f^2), Linf = max|f|, h^3 sum f, then
+ * (WAVE) the energy h^3 sum 1/2 (rho^2 + v.v), over the WHOLE grid.  nranks > 1: COLLECTIVE
+ * over all slabs of a chemora_grid_connect_ipc ring (every rank calls it at the same point
+ * of its call sequence): the per-rank partials are all-gathered through the peer-mapped
+ * workspaces (P - 1 ring rounds ordered by the same epoch flags as the step) and combined
+ * in rank order, so every rank returns the identical, deterministic result.  Synchronises.
+ * Returns CHEMORA_E_NONFINITE (after filling host_out) if this rank's state holds NaN/Inf;
+ * CHEMORA_E_PEER if nranks > 1 and the slab is not connected. */
 int chemora_norms(chemora_grid_t grid, double* host_out, void* stream);
 
-/* ---- multi-slab connectivity (z-slab ring, rank r's neighbours are r-1 and r+1 mod P) */
+/* ---- multi-slab connectivity (z-slab ring, rank r's neighbours are r-1 and r+1 mod P)
+ *
+ * The planned NCCL bootstrap (chemora_get_unique_id + an ncclUniqueId in the descriptor,
+ * SURVEY.md §8(b)) is replaced by peer memory: the halo exchange is
+ * fused into the stage kernels, which store their boundary planes straight into the
+ * neighbours' ghost planes through CUDA-IPC mappings of the neighbours' workspaces, and the
+ * phases are ordered by stream memory operations on epoch flags in the workspaces
+ * (DESIGN.md §6).  The only bootstrap data is the opaque per-rank peer record below, which
+ * the caller exchanges (e.g. torch.distributed.all_gather_object); no NCCL communicator
+ * exists.  The collective calls (chemora_rk4_step, chemora_halo_exchange,
+ * chemora_set_initial, chemora_upload_state, chemora_norms, chemora_constraint_norms,
+ * chemora_read_monitor) must be made by every rank in the same order. */
 
 /* Same-process slabs (emulation on one device): grids[r] has rank r of n. */
 int chemora_grid_connect_local(chemora_grid_t* grids, int32_t n);
@@ -193,6 +213,18 @@ int chemora_grid_connect_local(chemora_grid_t* grids, int32_t n);
 int chemora_peer_record_size(size_t* bytes);
 int chemora_grid_export_peer(chemora_grid_t grid, void* record_out);
 int chemora_grid_connect_ipc(chemora_grid_t grid, const void* record_lo, const void* record_hi);
+/* (The record also carries the system and kernel design; connect fails with CHEMORA_E_PEER
+ * if a neighbour's differ -- the step's phase count depends on the design.  After connect
+ * chemora_set_kernel_variant and chemora_autotune are refused.) */
+
+/* Optional host barrier after every phase of the cross-process protocol: fn(user) is called
+ * (after synchronising the stream) at the end of each phase, and must return only when every
+ * rank has reached the same point (e.g. a torch.distributed gloo barrier).  The stream waits
+ * of the next phase are then already satisfied when they reach the device, so no stream ever
+ * waits on another process's work -- required when several ranks share ONE device (their
+ * contexts are time-sliced), and a debugging aid otherwise.  fn = NULL restores the default
+ * (device-side ordering only). */
+int chemora_set_phase_barrier(chemora_grid_t grid, void (*fn)(void* user), void* user);
 
 /* ---- analysis and tuning */
 
@@ -207,9 +239,15 @@ int chemora_set_monitor(chemora_grid_t grid, int enable);
 
 /* Copy up to max per-step energies recorded since the last read (oldest first) to out;
  * *count receives the number copied.  Synchronises the stream.  The device ring holds 1024
- * steps; reading less often is an error (CHEMORA_E_INVALID). */
+ * steps; reading less often is an error (CHEMORA_E_INVALID).  nranks > 1 (IPC ring):
+ * COLLECTIVE, the values are the global energies (the slabs' values all-gathered and added
+ * in rank order), identical on every rank. */
 int chemora_read_monitor(chemora_grid_t grid, double* out, int32_t max, int32_t* count,
                          void* stream);
+/* The same for n same-process slabs (chemora_grid_connect_local): slab values added in slab
+ * order. */
+int chemora_read_monitor_multi(chemora_grid_t* grids, int32_t n, double* out, int32_t max,
+                               int32_t* count, void* stream);
 
 /* BSSN constraint monitors ("constraint equations"; SURVEY.md §8(f)
  * NEXT-3; reading R16), from the current state y with the RHS's 4th-order
@@ -225,8 +263,13 @@ int chemora_read_monitor(chemora_grid_t grid, double* out, int32_t max, int32_t*
  * given. */
 int chemora_constraints(chemora_grid_t grid, double* dev_fields, double* host_out, void* stream);
 
-/* nranks == 1: out[2q] = L2 = sqrt(h^3 sum c_q^2), out[2q+1] = Linf of the 7 constraints. */
+/* out[2q] = L2 = sqrt(h^3 sum c_q^2), out[2q+1] = Linf of the 7 constraints over the WHOLE
+ * grid; nranks > 1: collective like chemora_norms (rank-ordered combination). */
 int chemora_constraint_norms(chemora_grid_t grid, double* host_out, void* stream);
+/* Combine rank-major per-rank partials (nranks x 14: [sum c_q^2, max|c_q|] x 7, from
+ * chemora_constraints) in rank order into [L2, Linf] x 7. */
+int chemora_constraint_norms_combine(const chemora_grid_desc* desc, const double* partials,
+                                     int32_t nranks, double* out);
 
 /* Model-driven tiling choice ("autotuning is model driven"): a
  * footprint/occupancy model prunes the stage-kernel tilings to <= 4 candidates, each is

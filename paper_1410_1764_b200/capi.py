@@ -80,6 +80,10 @@ _SIGS = {
     "chemora_get_kernel_variant": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "chemora_read_monitor": ([_vp, _dp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
     "chemora_autotune": ([_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _dp, _vp], ctypes.c_int),
+    "chemora_read_monitor_multi": ([ctypes.POINTER(_vp), ctypes.c_int32, _dp, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
+    "chemora_set_phase_barrier": ([_vp, _vp, _vp], ctypes.c_int),
+    "chemora_constraint_norms_combine": ([_descp, _dp, ctypes.c_int32, _dp], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -281,6 +285,32 @@ def chemora_read_monitor(h, max_steps: int = 1024, stream=None) -> np.ndarray:
     _check(_lib.chemora_read_monitor(h, _dptr(out), max_steps, ctypes.byref(cnt), stream),
            "chemora_read_monitor")
     return out[:cnt.value].copy()
+
+
+def chemora_read_monitor_multi(handles, max_steps: int = 1024, stream=None) -> np.ndarray:
+    arr = (_vp * len(handles))(*handles)
+    out = np.zeros(max(1, max_steps))
+    cnt = ctypes.c_int32()
+    _check(_lib.chemora_read_monitor_multi(arr, len(handles), _dptr(out), max_steps, ctypes.byref(cnt), stream),
+           "chemora_read_monitor_multi")
+    return out[:cnt.value].copy()
+
+
+BARRIER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
+
+
+def chemora_set_phase_barrier(h, fn):
+    """fn: a BARRIER_FN (keep a reference alive while the handle uses it) or None."""
+    _check(_lib.chemora_set_phase_barrier(h, ctypes.cast(fn, _vp) if fn is not None else None, None),
+           "chemora_set_phase_barrier")
+
+
+def chemora_constraint_norms_combine(desc, partials: np.ndarray, nranks: int) -> np.ndarray:
+    partials = np.ascontiguousarray(partials, dtype=np.float64)
+    out = np.zeros(14)
+    _check(_lib.chemora_constraint_norms_combine(ctypes.byref(desc), _dptr(partials), nranks, _dptr(out)),
+           "chemora_constraint_norms_combine")
+    return out
 
 
 def chemora_autotune(h, trials: int = 3, stream=None):

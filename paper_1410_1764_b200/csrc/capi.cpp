@@ -44,6 +44,7 @@ struct PeerRecord {
   int32_t rank, nranks;
   int64_t local_extent[3];
   int32_t ghost, n_gf;
+  int32_t system, variant;  // neighbours must run the same kernel design (same phase count)
 };
 
 }  // namespace
@@ -79,6 +80,10 @@ struct chemora_grid_s {
   double* dtab;                 // BSSN derivative table (kBssnTab x interior points) or null
   uint64_t mon_written;         // steps recorded since creation
   uint64_t mon_read;            // steps already returned by chemora_read_monitor
+  double* gather;               // [nranks][kGatherLen] ring all-gather buffer (peer-read)
+  double* lo_gather;            // the lower neighbour's gather buffer (IPC mapping)
+  void (*barrier_fn)(void*);    // optional host barrier after every phase (shared device)
+  void* barrier_user;
 };
 
 namespace {
@@ -135,14 +140,15 @@ int norms_len(int system, int n_gf) { return 3 * n_gf + (system == CHEMORA_SYS_W
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
-// workspace: [sets][norm scratch][norm out][params][flags]
+// workspace: [sets][norm scratch][norm out][params][flags][monitor][table][gather]
 constexpr int kMonHist = 1024;  // energy-monitor ring (steps)
+constexpr int kGatherLen = kMonHist;  // doubles per rank slot of the collective gather
 constexpr int kBssnTab = 136;   // BSSN derivative-table slots per point (bssn_stage.cu variant 3)
 struct WsPlan {
-  size_t sets, scratch, out, params, flags, mon, hist, tab, total;
+  size_t sets, scratch, out, params, flags, mon, hist, tab, gather, total;
   int64_t mon_n;
 };
-WsPlan plan_ws(const Layout& L, int system) {
+WsPlan plan_ws(const Layout& L, int system, int nranks) {
   WsPlan p;
   const int len = norms_len(system, L.n_gf);
   p.sets = 0;
@@ -169,6 +175,9 @@ WsPlan plan_ws(const Layout& L, int system) {
   // BSSN: HBM derivative table of the table-fission kernels, [slot][interior point]
   p.tab = off;
   if (system == CHEMORA_SYS_BSSN) off += align256(sizeof(double) * (size_t)kBssnTab * L.nx * L.ny * L.nz);
+  // collective gather of per-rank results (chemora_norms & co. with nranks > 1)
+  p.gather = off;
+  if (nranks > 1) off += align256(sizeof(double) * (size_t)kGatherLen * nranks);
   p.total = off;
   return p;
 }
@@ -270,6 +279,45 @@ int phase_signal(chemora_grid_t g, cudaStream_t st) {
   CUresult r2 = g_write64((CUstream)st, (CUdeviceptr)g->hi_flag, g->epoch, 0);
   if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
     return fail(CHEMORA_E_PEER, "cuStreamWriteValue64 failed");
+  if (g->barrier_fn) {
+    // host-ordered phases (ranks sharing one device): the phase, flag writes included, is
+    // complete on this rank before any rank passes the barrier, so the next phase_wait is
+    // already satisfied when it reaches the device -- no stream ever waits on another
+    // process's work (chemora_set_phase_barrier)
+    CUDA_TRY(cudaStreamSynchronize(st));
+    g->barrier_fn(g->barrier_user);
+  }
+  return CHEMORA_OK;
+}
+
+// Ring all-gather of `len` doubles per rank (host src -> host out [nranks][len], rank-major),
+// over the peer-mapped gather buffers, P - 1 rounds ordered by the phase flags: in round t
+// rank r copies slot (r - t) mod P from its lower neighbour, which received it in round
+// t - 1.  Every rank ends with the same rows in rank order, so the rank-ordered combination
+// that follows is deterministic and identical everywhere.  Synchronises the stream.
+int ring_allgather(chemora_grid_t g, const double* host_src, int len, double* host_out, cudaStream_t st) {
+  const int P = g->desc.nranks, r = g->desc.rank;
+  if (len > kGatherLen) return fail(CHEMORA_E_INVALID, "gather length too large");
+  if (P == 1) {
+    memcpy(host_out, host_src, sizeof(double) * len);
+    return CHEMORA_OK;
+  }
+  if (!g->ipc || !g->lo_gather) return fail(CHEMORA_E_PEER, "nranks > 1: connect the slabs with chemora_grid_connect_ipc first");
+  if (int rc = phase_wait(g, st)) return rc;  // neighbours finished reading our buffer
+  CUDA_TRY(cudaMemcpyAsync(g->gather + (size_t)r * kGatherLen, host_src, sizeof(double) * len,
+                           cudaMemcpyHostToDevice, st));
+  if (int rc = phase_signal(g, st)) return rc;
+  for (int t = 1; t < P; ++t) {
+    if (int rc = phase_wait(g, st)) return rc;
+    const size_t slot = (size_t)((r - t + P) % P) * kGatherLen;
+    CUDA_TRY(cudaMemcpyAsync(g->gather + slot, g->lo_gather + slot, sizeof(double) * len,
+                             cudaMemcpyDeviceToDevice, st));
+    if (int rc = phase_signal(g, st)) return rc;
+  }
+  for (int q = 0; q < P; ++q)
+    CUDA_TRY(cudaMemcpyAsync(host_out + (size_t)q * len, g->gather + (size_t)q * kGatherLen,
+                             sizeof(double) * len, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
   return CHEMORA_OK;
 }
 
@@ -375,7 +423,7 @@ int chemora_grid_required_bytes(const chemora_grid_desc* desc, size_t* bytes) {
   int rc = validate(desc);
   if (rc) return rc;
   if (!bytes) return fail(CHEMORA_E_INVALID, "bytes is NULL");
-  *bytes = plan_ws(layout_of(*desc), desc->system).total;
+  *bytes = plan_ws(layout_of(*desc), desc->system, desc->nranks).total;
   return CHEMORA_OK;
 }
 
@@ -387,7 +435,7 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   if (!ws) return fail(CHEMORA_E_INVALID, "workspace is NULL");
   if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(CHEMORA_E_NOMEM, "workspace must be 256-byte aligned");
   const Layout L = layout_of(*desc);
-  const WsPlan P = plan_ws(L, desc->system);
+  const WsPlan P = plan_ws(L, desc->system, desc->nranks);
   if (bytes < P.total)
     return fail(CHEMORA_E_NOMEM, "workspace has " + std::to_string(bytes) + " bytes, needs " + std::to_string(P.total));
   DeviceGuard dg(desc->device);
@@ -416,6 +464,10 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->mon_hist = reinterpret_cast<double*>(g->ws + P.hist);
   g->mon_written = 0;
   g->mon_read = 0;
+  g->gather = reinterpret_cast<double*>(g->ws + P.gather);
+  g->lo_gather = nullptr;
+  g->barrier_fn = nullptr;
+  g->barrier_user = nullptr;
   auto* fl = reinterpret_cast<unsigned long long*>(g->ws + P.flags);
   g->nan_flag = fl;
   g->flags = fl + 1;
@@ -492,6 +544,10 @@ static int set_initial_nofill(chemora_grid_t g, int kind, const double* host_src
                               uint64_t seed, cudaStream_t st) {
   DeviceGuard dg(g->desc.device);
   const Layout& L = g->L;
+  // z-slabs in other processes: the neighbours' previous phase may still store into our
+  // ghost planes, which the clear below overwrites -- wait for it first; and publish the
+  // end of the clear (phase_signal below) before anyone pushes the new ghosts into us
+  if (int rc = phase_wait(g, st)) return rc;
   switch (kind) {
     case CHEMORA_INIT_HOST:
     case CHEMORA_INIT_HOST_PADDED: {
@@ -545,7 +601,7 @@ static int set_initial_nofill(chemora_grid_t g, int kind, const double* host_src
   CUDA_TRY(cudaMemcpyAsync(g->nan_flag, &nf, sizeof(nf), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   g->step = 0;
-  return CHEMORA_OK;
+  return phase_signal(g, st);
 }
 
 int chemora_set_initial(chemora_grid_t g, int kind, const double* host_src, const double* kp,
@@ -685,6 +741,10 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
 
 int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* ms_out, void* stream) {
   if (int rc = check_grid(g)) return rc;
+  // the trial launches store ghost images into the neighbours' sets outside the phase
+  // protocol, and ranks timing independently could pick different designs: tune before
+  // chemora_grid_connect_ipc (the record carries the design, connect refuses a mismatch)
+  if (g->ipc) return fail(CHEMORA_E_PEER, "autotune a z-slab before chemora_grid_connect_ipc");
   if (trials < 1) trials = 3;
   DeviceGuard dg(g->desc.device);
   cudaStream_t st = as_stream(stream);
@@ -794,7 +854,45 @@ int chemora_read_monitor(chemora_grid_t g, double* out, int32_t max, int32_t* co
   for (int32_t i = 0; i < n; ++i) out[i] = ring[(g->mon_read + i) % kMonHist];
   g->mon_read += n;
   *count = n;
+  const int P = g->desc.nranks;
+  if (P > 1 && n > 0) {
+    // collective: the global energy of each step is the sum of the slabs' values, added in
+    // rank order (every rank gets the same values; ranks step in lockstep, so n agrees)
+    std::vector<double> all((size_t)n * P);
+    if (int rc = ring_allgather(g, out, n, all.data(), st)) return rc;
+    for (int32_t i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int r = 0; r < P; ++r) s += all[(size_t)r * n + i];
+      out[i] = s;
+    }
+  }
   return read_nan_flag(g, st);
+}
+
+int chemora_read_monitor_multi(chemora_grid_t* grids, int32_t n, double* out, int32_t max, int32_t* count,
+                               void* stream) {
+  if (!grids || n < 1 || !count || (max > 0 && !out)) return fail(CHEMORA_E_INVALID, "bad arguments");
+  std::vector<double> part((size_t)(max > 0 ? max : 1));
+  int32_t cnt0 = -1;
+  int status = CHEMORA_OK;
+  for (int r = 0; r < n; ++r) {
+    int32_t c = 0;
+    int rc = chemora_read_monitor(grids[r], part.data(), max, &c, stream);
+    if (rc && rc != CHEMORA_E_NONFINITE) return rc;
+    if (rc) status = rc;
+    if (cnt0 >= 0 && c != cnt0) return fail(CHEMORA_E_PEER, "slabs recorded different step counts");
+    for (int32_t i = 0; i < c; ++i) out[i] = (r == 0 ? 0.0 : out[i]) + part[i];  // slab order
+    cnt0 = c;
+  }
+  *count = cnt0;
+  return status;
+}
+
+int chemora_set_phase_barrier(chemora_grid_t g, void (*fn)(void*), void* user) {
+  if (int rc = check_grid(g)) return rc;
+  g->barrier_fn = fn;
+  g->barrier_user = user;
+  return CHEMORA_OK;
 }
 
 int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t nsteps, void* stream) {
@@ -897,12 +995,16 @@ int chemora_norms_combine(const chemora_grid_desc* d, const double* partials, in
 
 int chemora_norms(chemora_grid_t g, double* out, void* stream) {
   if (int rc = check_grid(g)) return rc;
-  if (g->desc.nranks > 1)
-    return fail(CHEMORA_E_UNSUPPORTED, "nranks > 1: gather chemora_norms_partial and call chemora_norms_combine");
-  std::vector<double> part(norms_len(g->desc.system, g->L.n_gf));
+  if (!out) return fail(CHEMORA_E_INVALID, "out is NULL");
+  const int len = norms_len(g->desc.system, g->L.n_gf), P = g->desc.nranks;
+  std::vector<double> part(len), all((size_t)len * P);
   int rc = chemora_norms_partial(g, part.data(), stream);
   if (rc && rc != CHEMORA_E_NONFINITE) return rc;
-  int rc2 = chemora_norms_combine(&g->desc, part.data(), 1, out);
+  const std::string nonfinite = rc ? g_err : std::string();
+  DeviceGuard dg(g->desc.device);
+  if (int rc1 = ring_allgather(g, part.data(), len, all.data(), as_stream(stream))) return rc1;
+  int rc2 = chemora_norms_combine(&g->desc, all.data(), P, out);
+  if (rc && !rc2) g_err = nonfinite;
   return rc ? rc : rc2;
 }
 
@@ -919,16 +1021,36 @@ int chemora_constraints(chemora_grid_t g, double* fields, double* out, void* str
   return read_nan_flag(g, st);
 }
 
+int chemora_constraint_norms_combine(const chemora_grid_desc* d, const double* partials, int32_t nranks,
+                                     double* out) {
+  if (!d || !partials || !out || nranks < 1) return fail(CHEMORA_E_INVALID, "bad arguments");
+  const double vol = d->spacing[0] * d->spacing[1] * d->spacing[2];
+  for (int q = 0; q < 7; ++q) {
+    double s = 0.0, m = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+      s += partials[(size_t)r * 14 + 2 * q];
+      m = std::fmax(m, partials[(size_t)r * 14 + 2 * q + 1]);
+    }
+    out[2 * q] = std::sqrt(vol * s);
+    out[2 * q + 1] = m;
+  }
+  return CHEMORA_OK;
+}
+
 int chemora_constraint_norms(chemora_grid_t g, double* out, void* stream) {
   if (int rc = check_grid(g)) return rc;
   if (!out) return fail(CHEMORA_E_INVALID, "out is NULL");
-  if (g->desc.nranks > 1)
-    return fail(CHEMORA_E_UNSUPPORTED, "nranks > 1: gather chemora_constraints partials");
-  int rc = chemora_constraints(g, nullptr, out, stream);
+  const int P = g->desc.nranks;
+  double part[14];
+  int rc = chemora_constraints(g, nullptr, part, stream);
   if (rc && rc != CHEMORA_E_NONFINITE) return rc;
-  const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
-  for (int q = 0; q < 7; ++q) out[2 * q] = std::sqrt(vol * out[2 * q]);
-  return rc;
+  const std::string nonfinite = rc ? g_err : std::string();
+  std::vector<double> all((size_t)14 * P);
+  DeviceGuard dg(g->desc.device);
+  if (int rc1 = ring_allgather(g, part, 14, all.data(), as_stream(stream))) return rc1;
+  int rc2 = chemora_constraint_norms_combine(&g->desc, all.data(), P, out);
+  if (rc && !rc2) g_err = nonfinite;
+  return rc ? rc : rc2;
 }
 
 int chemora_grid_connect_local(chemora_grid_t* grids, int32_t n) {
@@ -973,6 +1095,8 @@ int chemora_grid_export_peer(chemora_grid_t g, void* rec_out) {
   rec.local_extent[0] = g->L.nx; rec.local_extent[1] = g->L.ny; rec.local_extent[2] = g->L.nz;
   rec.ghost = g->L.g;
   rec.n_gf = g->L.n_gf;
+  rec.system = g->desc.system;
+  rec.variant = g->variant;
   memcpy(rec_out, &rec, sizeof(rec));
   return CHEMORA_OK;
 }
@@ -990,8 +1114,12 @@ int chemora_grid_connect_ipc(chemora_grid_t g, const void* rlo, const void* rhi)
     if (p->local_extent[0] != g->L.nx || p->local_extent[1] != g->L.ny ||
         p->local_extent[2] != g->L.nz || p->ghost != g->L.g || p->n_gf != g->L.n_gf)
       return fail(CHEMORA_E_PEER, "neighbour layout differs");
+  for (const PeerRecord* p : {&lo, &hi})
+    if (p->system != g->desc.system || p->variant != g->variant)
+      return fail(CHEMORA_E_PEER, "neighbour runs a different system or kernel design (variant " +
+                                      std::to_string(p->variant) + " vs " + std::to_string(g->variant) + ")");
   DeviceGuard dg(g->desc.device);
-  const WsPlan P = plan_ws(g->L, g->desc.system);
+  const WsPlan P = plan_ws(g->L, g->desc.system, g->desc.nranks);
   auto open = [&](const PeerRecord& rec, char** base) -> int {
     void* p = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&p, rec.handle, cudaIpcMemLazyEnablePeerAccess);
@@ -1020,6 +1148,7 @@ int chemora_grid_connect_ipc(chemora_grid_t g, const void* rlo, const void* rhi)
   // we signal the lower neighbour in its flags[1] ("from hi") and the upper in flags[0]
   g->lo_flag = reinterpret_cast<unsigned long long*>(blo + P.flags) + 2;
   g->hi_flag = reinterpret_cast<unsigned long long*>(bhi + P.flags) + 1;
+  g->lo_gather = reinterpret_cast<double*>(blo + P.gather);
   g->ipc = true;
   g->epoch = 0;
   return CHEMORA_OK;

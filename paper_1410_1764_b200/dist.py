@@ -1,10 +1,10 @@
 """Multi-rank plumbing over torch.distributed (process groups only; no arithmetic of the
 method): the z-slab ring topology (PAPER.md:200-204 driver decomposition), the exchange of
-the per-rank peer records that connect neighbouring slabs, and the gather of per-rank norm
-partials that the C library combines in rank order (chemora_norms_combine)."""
+the opaque per-rank peer records that connect neighbouring slabs, and the host barrier the
+library calls between phases when ranks share one device.  Every reduction over ranks
+(norms, constraint norms, monitor energies) is done by the C library itself
+(chemora_norms & co. are collective over the peer-mapped workspaces)."""
 from __future__ import annotations
-
-import numpy as np
 
 
 def ring_neighbours(rank: int, world: int) -> tuple[int, int]:
@@ -30,35 +30,10 @@ def exchange_records(record: bytes, rank: int, world: int, group=None) -> tuple[
     return allrec[lo], allrec[hi]
 
 
-def gather_partials(partials: np.ndarray, world: int, group=None) -> np.ndarray:
-    """all_gather per-rank norm partials; rows in rank order (deterministic combine)."""
+def barrier_callback(group=None):
+    """The host barrier chemora_set_phase_barrier calls after every phase."""
     import torch.distributed as dist
-    out = [None] * world
-    dist.all_gather_object(out, np.asarray(partials, dtype=np.float64).tolist(), group=group)
-    return np.array(out, dtype=np.float64)
 
-
-def combine_constraint_partials(gathered: np.ndarray, vol: float) -> np.ndarray:
-    """Rank-major [world][14] partials [sum c_q^2, max |c_q|] x 7 of chemora_constraints ->
-    [L2_q, Linf_q] x 7 (sums in rank order, so the result is deterministic)."""
-    g = np.asarray(gathered, dtype=np.float64).reshape(-1, 14)
-    out = np.zeros(14)
-    for q in range(7):
-        s = 0.0
-        for r in range(g.shape[0]):
-            s += g[r, 2 * q]
-        out[2 * q] = np.sqrt(vol * s)
-        out[2 * q + 1] = g[:, 2 * q + 1].max()
-    return out
-
-
-def sum_in_rank_order(gathered: np.ndarray) -> np.ndarray:
-    """Rank-major [world][n] per-slab values (e.g. monitor energies) -> their sums over the
-    slabs, added in rank order (deterministic)."""
-    g = np.asarray(gathered, dtype=np.float64)
-    if g.ndim == 1:
-        g = g[:, None]
-    out = np.zeros(g.shape[1])
-    for r in range(g.shape[0]):
-        out = out + g[r]
-    return out
+    def _barrier(_user):
+        dist.barrier(group=group)
+    return _barrier

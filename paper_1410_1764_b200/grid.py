@@ -81,12 +81,9 @@ class Grid:
     def halo_exchange(self):
         C.chemora_halo_exchange(self.handle, self.stream)
 
-    def norms(self, group=None):
-        if self.nranks == 1:
-            return C.chemora_norms(self.handle, self.system, self.stream)
-        part = C.chemora_norms_partial(self.handle, self.system, self.stream)
-        gathered = D.gather_partials(part, self.nranks, group)
-        return C.chemora_norms_combine(self.desc, gathered, self.nranks)
+    def norms(self):
+        """Global norms (collective over the IPC-connected slabs when nranks > 1)."""
+        return C.chemora_norms(self.handle, self.system, self.stream)
 
     def constraints(self, out: torch.Tensor | None = None) -> torch.Tensor:
         """BSSN constraint fields [H, M1, M2, M3, G1, G2, G3][z][y][x] of the current state."""
@@ -97,20 +94,20 @@ class Grid:
         C.chemora_constraints(self.handle, out.data_ptr(), False, self.stream)
         return out
 
-    def constraint_norms(self, group=None) -> np.ndarray:
-        """[L2, Linf] of H, M1..3, G1..3 (14 doubles), over all ranks."""
-        if self.nranks == 1:
-            return C.chemora_constraint_norms(self.handle, self.stream)
-        part = C.chemora_constraints(self.handle, None, True, self.stream)
-        gathered = D.gather_partials(part, self.nranks, group)
-        h = self.desc.spacing
-        return D.combine_constraint_partials(gathered, h[0] * h[1] * h[2])
+    def constraint_norms(self) -> np.ndarray:
+        """[L2, Linf] of H, M1..3, G1..3 (14 doubles), over all ranks (collective)."""
+        return C.chemora_constraint_norms(self.handle, self.stream)
 
-    def connect_ipc(self, group=None):
-        """Exchange peer records over torch.distributed and open the ring neighbours."""
+    def connect_ipc(self, group=None, host_barrier=False):
+        """Exchange peer records over torch.distributed and open the ring neighbours.
+        host_barrier: end every phase with a stream sync + torch.distributed barrier
+        (chemora_set_phase_barrier) -- required when ranks share one device."""
         rec = C.chemora_grid_export_peer(self.handle)
         lo, hi = D.exchange_records(rec, self.rank, self.nranks, group)
         C.chemora_grid_connect_ipc(self.handle, lo, hi)
+        if host_barrier:
+            self._barrier = C.BARRIER_FN(D.barrier_callback(group))
+            C.chemora_set_phase_barrier(self.handle, self._barrier)
 
     def set_kernel_variant(self, v):
         C.chemora_set_kernel_variant(self.handle, v)
@@ -123,14 +120,9 @@ class Grid:
     def set_monitor(self, enable=True):
         C.chemora_set_monitor(self.handle, enable)
 
-    def read_monitor(self, max_steps=1024, group=None):
-        """Per-step energies since the last read; with nranks > 1 the slab energies are
-        gathered and summed in rank order (every rank gets the global values)."""
-        e = C.chemora_read_monitor(self.handle, max_steps, self.stream)
-        if self.nranks == 1:
-            return e
-        gathered = D.gather_partials(np.asarray(e, dtype=np.float64), self.nranks, group)
-        return D.sum_in_rank_order(gathered)
+    def read_monitor(self, max_steps=1024):
+        """Per-step energies since the last read (global values, collective when nranks > 1)."""
+        return C.chemora_read_monitor(self.handle, max_steps, self.stream)
 
     def autotune(self, trials=3):
         return C.chemora_autotune(self.handle, trials, self.stream)
@@ -192,8 +184,7 @@ class LocalSlabs:
 
     def read_monitor(self, max_steps=1024):
         """Per-step global energies: the slabs' fused-monitor values summed in slab order."""
-        parts = [C.chemora_read_monitor(g.handle, max_steps, self.stream) for g in self.grids]
-        return D.sum_in_rank_order(np.array(parts, dtype=np.float64))
+        return C.chemora_read_monitor_multi(self.handles, max_steps, self.stream)
 
     def close(self):
         for g in self.grids:

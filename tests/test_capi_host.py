@@ -120,14 +120,15 @@ def test_norms_combine_host_logic():
 
 def test_combine_constraint_partials():
     """Rank-major constraint partials -> L2 = sqrt(h^3 sum), Linf = max over ranks."""
+    _ensure_built()
     import numpy as np
-    from paper_1410_1764_b200 import dist as D
+    from paper_1410_1764_b200 import capi as C
     parts = np.zeros((2, 14))
     parts[0, 0::2] = np.arange(7) + 1.0
     parts[1, 0::2] = 2.0 * (np.arange(7) + 1.0)
     parts[0, 1::2] = 0.5
     parts[1, 1::2] = np.linspace(0.1, 0.9, 7)
-    out = D.combine_constraint_partials(parts.ravel(), 0.125)
+    out = C.chemora_constraint_norms_combine(_desc(system=C.SYS_BSSN, spacing=(0.5, 0.5, 0.5)), parts, 2)
     assert np.allclose(out[0::2], np.sqrt(0.125 * 3.0 * (np.arange(7) + 1.0)), rtol=1e-15)
     assert np.array_equal(out[1::2], np.maximum(0.5, np.linspace(0.1, 0.9, 7)))
 
@@ -145,12 +146,3 @@ def test_missing_library_fails_loudly(tmp_path):
     assert r.returncode != 0
     assert "is missing" in r.stderr and "no CPU fallback" in r.stderr
 
-
-def test_sum_in_rank_order():
-    """Per-slab monitor energies, rank-major -> per-step sums added in rank order."""
-    import numpy as np
-    from paper_1410_1764_b200 import dist as D
-    parts = np.array([[1.0, 2.0, 3.0], [0.5, 0.25, 0.125], [1e-17, 0.0, 1.0]])
-    out = D.sum_in_rank_order(parts)
-    assert np.array_equal(out, (parts[0] + parts[1]) + parts[2])
-    assert np.array_equal(D.sum_in_rank_order(np.array([2.0, 3.0])), np.array([5.0]))

@@ -1,7 +1,8 @@
 """World-size 2 and 3 CPU tests (gloo) of the multi-rank host logic: ring topology, slab
-bounds, the peer-record exchange that connects neighbouring z-slabs, and the rank-ordered
-combination of norm partials.  (The device side of the N>1 path -- stage kernels storing
-into peer ghost planes -- is covered by the single-device slab emulation GPU tests.)"""
+bounds, the peer-record exchange that connects neighbouring z-slabs, the host phase barrier,
+and the C library's rank-ordered combination of per-rank partials.  (The device side of the
+N>1 path -- stage kernels storing into peer ghost planes, the collective norms over peer
+memory -- runs in tests/test_gpu_ipc_procs.py: 2 and 3 processes on one GPU.)"""
 from __future__ import annotations
 
 import os
@@ -70,6 +71,13 @@ def test_peer_record_exchange_ring(world):
         assert res[0][0] == res[0][1]
 
 
+def _gather(part, world):
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, np.asarray(part, dtype=np.float64).tolist())
+    return np.array(out, dtype=np.float64)
+
+
 def _norms(rank, world):
     """Each rank owns a z-slab of one global field; partials computed here in numpy, then
     gathered and combined by the C library in rank order."""
@@ -85,7 +93,7 @@ def _norms(rank, world):
         part[3 * f + 1] = np.abs(sl[f]).max()
         part[3 * f + 2] = sl[f].sum()
     part[15] = 0.5 * (sl[1:] ** 2).sum()
-    gathered = D.gather_partials(part, world)
+    gathered = _gather(part, world)
     desc = C.make_desc(C.SYS_WAVE, (7, 6, 12), (0.5, 0.5, 0.5), rank=rank, nranks=world)
     combined = C.chemora_norms_combine(desc, gathered, world)
     return combined.tolist(), gathered[:, 0].tolist()
@@ -113,7 +121,9 @@ def test_norm_partials_combine_in_rank_order(world):
 
 def _constraints(rank, world):
     """Constraint-monitor partials [sum c^2, max |c|] x 7 of each rank's slab, gathered and
-    combined on every rank (the host half of Grid.constraint_norms for nranks > 1)."""
+    combined on every rank by chemora_constraint_norms_combine (the combine step of the
+    collective chemora_constraint_norms)."""
+    from paper_1410_1764_b200 import capi as C
     from paper_1410_1764_b200 import dist as D
     rng = np.random.default_rng(7)
     c = rng.standard_normal((7, 12, 5, 6))
@@ -123,8 +133,9 @@ def _constraints(rank, world):
     for q in range(7):
         part[2 * q] = (sl[q] ** 2).sum()
         part[2 * q + 1] = np.abs(sl[q]).max()
-    gathered = D.gather_partials(part, world)
-    return D.combine_constraint_partials(gathered, 0.25).tolist()
+    gathered = _gather(part, world)
+    desc = C.make_desc(C.SYS_BSSN, (6, 5, 12), (0.25, 1.0, 1.0), rank=rank, nranks=world)
+    return C.chemora_constraint_norms_combine(desc, gathered, world).tolist()
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -153,3 +164,31 @@ def test_slab_bounds_and_validation():
         D.slab_bounds(1000, 3, 0)
     assert D.ring_neighbours(0, 4) == (3, 1)
     assert D.ring_neighbours(3, 4) == (2, 0)
+
+
+def _barrier_cb(rank, world):
+    """The phase-barrier callback the library calls between phases is a real barrier: no
+    rank leaves round k before every rank has entered it."""
+    import time
+    import torch.distributed as dist
+    from paper_1410_1764_b200 import dist as D
+    cb = D.barrier_callback()
+    seen = []
+    for k in range(3):
+        time.sleep(0.05 * ((rank + k) % world))
+        t = time.time()
+        cb(None)
+        seen.append(t)
+    allt = [None] * world
+    dist.all_gather_object(allt, seen)
+    return allt
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_phase_barrier_callback(world):
+    res = _run(world, "_barrier_cb")
+    allt = res[0]
+    # entry times of round k of every rank precede ... (ordering checked through exits:
+    # each rank records its entry time; all ranks' round-k entries precede any round-(k+1) entry)
+    for k in range(2):
+        assert max(t[k] for t in allt) <= min(t[k + 1] for t in allt)
