@@ -155,6 +155,17 @@ def norms(system: int, interior: np.ndarray, spacing, g: int = DEFAULT_GHOST) ->
 CONSTRAINT_NAMES = ("H", "M1", "M2", "M3", "G1", "G2", "G3")
 
 
+def constraints_padded(padded: np.ndarray, spacing, g: int = DEFAULT_GHOST) -> np.ndarray:
+    """BSSN constraint fields at interior points, ghosts of ``padded`` used as they are."""
+    padded = np.ascontiguousarray(padded, dtype=np.float64)
+    n = (padded.shape[3] - 2 * g, padded.shape[2] - 2 * g, padded.shape[1] - 2 * g)
+    out = np.zeros((7, n[2], n[1], n[0]))
+    rc = lib().chemora_oracle_constraints(_dp(padded), _ext(n), g, _sp(spacing), _dp(out))
+    if rc:
+        raise ValueError(f"oracle constraints rc={rc}")
+    return out
+
+
 def constraints(interior: np.ndarray, spacing, g: int = DEFAULT_GHOST) -> np.ndarray:
     """BSSN constraint fields [H, M1..3, G1..3] on a periodic grid, shape [7][Nz][Ny][Nx]."""
     y = fill_ghosts(pad(np.ascontiguousarray(interior, dtype=np.float64), g), g)

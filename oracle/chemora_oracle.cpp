@@ -430,7 +430,9 @@ void bssn_rhs(const double* y, double* kout, const Grid& G, const double* prm) {
 // Vacuum constraints of the BSSN variables (PAPER.md:472-473
 // "constraint equations"), evaluated with the same 4th-order stencils:
 //   H   = R + 2/3 K^2 - At_ij At^ij,   R = e^{-4 phi} gt^ij (R~_ij + R^phi_ij)   (App. A.2)
-//   M^i = d_j At^ij + Gt^i_jk At^jk + 6 At^ij d_j phi - 2/3 gt^ij d_j K
+//   M^i = D~_j At^ij + 6 At^ij d_j phi - 2/3 gt^ij d_j K,
+//         D~_j At^ij = d_j At^ij + Gt^i_jk At^jk + Gt^j_jk At^ik  (full conformal covariant
+//         divergence: det gt is computed, not assumed 1 -- App. A.2; R16)
 //   G^i = Xt^i - gt^jk Gt^i_jk
 // out: 7 interior fields [H, M1, M2, M3, G1, G2, G3].
 void bssn_constraints(const double* y, double* out, const Grid& G) {
@@ -556,6 +558,8 @@ void bssn_constraints(const double* y, double* out, const Grid& G) {
           double m = div;
           for (int j = 0; j < 3; ++j)
             for (int kx = 0; kx < 3; ++kx) m += Gu[i][j][kx] * Atu[j][kx];
+          for (int j = 0; j < 3; ++j)
+            for (int kx = 0; kx < 3; ++kx) m += Gu[j][j][kx] * Atu[i][kx];
           for (int j = 0; j < 3; ++j) m += 6.0 * Atu[i][j] * dphi[j] - (2.0 / 3.0) * gu[i][j] * dtrK[j];
           out[(1 + i) * ni + o] = m;
           out[(4 + i) * ni + o] = Xt[i] - Xtn[i];

@@ -438,7 +438,8 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
 // Vacuum BSSN constraints (R16) with
 // the RHS's stencils and Ricci tensor:
 //   c[0] = H   = e^{-4 phi} gt^ij (R~_ij + R^phi_ij) + 2/3 K^2 - At_ij At^ij
-//   c[1+i] = M^i = d_j At^ij + Gt^i_jk At^jk + 6 At^ij d_j phi - 2/3 gt^ij d_j K
+//   c[1+i] = M^i = d_j At^ij + Gt^i_jk At^jk + Gt^j_jk At^ik + 6 At^ij d_j phi - 2/3 gt^ij d_j K
+//            (the full conformal divergence D~_j At^ij: det gt is not assumed 1)
 //   c[4+i] = G^i = Xt^i - gt^jk Gt^i_jk
 // d_j At^ij by the product rule with d_j gt^ab = -gt^ac (d_j gt_cd) gt^db.
 __device__ __forceinline__ void bssn_constraint_point(const StencilP& D, const BssnK& K, double* c) {
@@ -564,11 +565,15 @@ __device__ __forceinline__ void bssn_constraint_point(const StencilP& D, const B
         V[l] = fma(gu[sy(j, k)], dg[j][sy(k, l)], V[l]);    // gt^jk d_j gt_kl
       }
   }
+  double Gjjk[3];  // Gt^j_jk
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Gjjk[k] = Gu[0][sy(0, k)] + Gu[1][sy(1, k)] + Gu[2][sy(2, k)];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     double m = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
+      m = fma(Gjjk[k], Au[sy(i, k)], m);
       m = fma(gu[sy(i, k)], W[k] - U[k], m);
       m = fma(-Au[sy(i, k)], V[k], m);
       m = fma(6.0 * Au[sy(i, k)], dphi[k], m);

@@ -839,11 +839,11 @@ int chemora_set_monitor(chemora_grid_t g, int enable) {
   return CHEMORA_OK;
 }
 
-int chemora_read_monitor(chemora_grid_t g, double* out, int32_t max, int32_t* count, void* stream) {
+// This slab's per-step energies since the last read (no collective).
+static int read_monitor_local(chemora_grid_t g, double* out, int32_t max, int32_t* count, cudaStream_t st) {
   if (int rc = check_grid(g)) return rc;
   if (!count || (max > 0 && !out)) return fail(CHEMORA_E_INVALID, "bad output buffer");
   DeviceGuard dg(g->desc.device);
-  cudaStream_t st = as_stream(stream);
   CUDA_TRY(cudaStreamSynchronize(st));
   const uint64_t avail = g->mon_written - g->mon_read;
   if (avail > (uint64_t)kMonHist)
@@ -854,19 +854,33 @@ int chemora_read_monitor(chemora_grid_t g, double* out, int32_t max, int32_t* co
   for (int32_t i = 0; i < n; ++i) out[i] = ring[(g->mon_read + i) % kMonHist];
   g->mon_read += n;
   *count = n;
+  return read_nan_flag(g, st);
+}
+
+int chemora_read_monitor(chemora_grid_t g, double* out, int32_t max, int32_t* count, void* stream) {
+  if (int rc = check_grid(g)) return rc;
   const int P = g->desc.nranks;
+  if (P > 1 && !g->ipc)
+    return fail(CHEMORA_E_PEER, "same-process slabs: read the global energies with chemora_read_monitor_multi");
+  cudaStream_t st = as_stream(stream);
+  int rc = read_monitor_local(g, out, max, count, st);
+  if (rc && rc != CHEMORA_E_NONFINITE) return rc;
+  const int32_t n = *count;
   if (P > 1 && n > 0) {
     // collective: the global energy of each step is the sum of the slabs' values, added in
     // rank order (every rank gets the same values; ranks step in lockstep, so n agrees)
+    const std::string nonfinite = rc ? g_err : std::string();
     std::vector<double> all((size_t)n * P);
-    if (int rc = ring_allgather(g, out, n, all.data(), st)) return rc;
+    DeviceGuard dg(g->desc.device);
+    if (int rc1 = ring_allgather(g, out, n, all.data(), st)) return rc1;
     for (int32_t i = 0; i < n; ++i) {
       double s = 0.0;
       for (int r = 0; r < P; ++r) s += all[(size_t)r * n + i];
       out[i] = s;
     }
+    if (rc) g_err = nonfinite;
   }
-  return read_nan_flag(g, st);
+  return rc;
 }
 
 int chemora_read_monitor_multi(chemora_grid_t* grids, int32_t n, double* out, int32_t max, int32_t* count,
@@ -877,7 +891,7 @@ int chemora_read_monitor_multi(chemora_grid_t* grids, int32_t n, double* out, in
   int status = CHEMORA_OK;
   for (int r = 0; r < n; ++r) {
     int32_t c = 0;
-    int rc = chemora_read_monitor(grids[r], part.data(), max, &c, stream);
+    int rc = read_monitor_local(grids[r], part.data(), max, &c, as_stream(stream));
     if (rc && rc != CHEMORA_E_NONFINITE) return rc;
     if (rc) status = rc;
     if (cnt0 >= 0 && c != cnt0) return fail(CHEMORA_E_PEER, "slabs recorded different step counts");
