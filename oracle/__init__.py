@@ -23,7 +23,8 @@ WAVE, BSSN = 1, 2
 N_GF = {WAVE: 5, BSSN: 25}
 DEFAULT_GHOST = 3
 
-_lib = None
+_LIB_FMA = os.path.join(_HERE, "liboracle_fma.so")
+_libs = {}
 
 
 def build(force: bool = False) -> str:
@@ -36,11 +37,52 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
-def lib():
+def build_fma(force: bool = False) -> str:
+    """The SAME source built with FMA contraction (-mfma -ffp-contract=fast): a second,
+    equally legitimate rounding sequence of the same arithmetic.  Its difference from the
+    plain build is the oracle's own rounding-noise floor, the scale
+    against which GPU-vs-oracle differences at large grids are read."""
+    if force or not os.path.exists(_LIB_FMA) or os.path.getmtime(_LIB_FMA) < os.path.getmtime(_SRC):
+        cmd = ["g++", "-O2", "-std=c++17", "-fopenmp", "-mfma", "-ffp-contract=fast", "-fno-fast-math",
+               "-shared", "-fPIC", "-o", _LIB_FMA + ".tmp", _SRC]
+        subprocess.check_call(cmd)
+        os.replace(_LIB_FMA + ".tmp", _LIB_FMA)
+    return _LIB_FMA
+
+
+def host_has_fma() -> bool:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            return any(line.startswith("flags") and " fma " in line + " " for line in fh)
+    except OSError:
+        return False
+
+
+class use_fma_build:
+    """Context manager: oracle calls inside use the FMA-contracted build (noise floor)."""
+
+    def __enter__(self):
+        global _lib
+        self._saved = _lib
+        _lib = lib("fma")
+        return self
+
+    def __exit__(self, *a):
+        global _lib
+        _lib = self._saved
+
+
+_lib = None
+
+
+def lib(kind: str = ""):
     global _lib
-    if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB)
+    if kind == "" and _lib is not None:
+        return _lib
+    key = kind or "plain"
+    if key not in _libs:
+        path = build_fma() if kind == "fma" else build()
+        L = ctypes.CDLL(path)
         dp = ctypes.POINTER(ctypes.c_double)
         i64p = ctypes.POINTER(ctypes.c_int64)
         L.chemora_oracle_fill_ghosts.argtypes = [dp, ctypes.c_int, i64p, ctypes.c_int]
@@ -51,8 +93,10 @@ def lib():
         L.chemora_oracle_norms.argtypes = [ctypes.c_int, dp, i64p, ctypes.c_int, dp, dp]
         L.chemora_oracle_default_bssn_params.argtypes = [dp]
         L.chemora_oracle_constraints.argtypes = [dp, i64p, ctypes.c_int, dp, dp]
-        _lib = L
-    return _lib
+        _libs[key] = L
+    if kind == "":
+        _lib = _libs[key]
+    return _libs[key]
 
 
 def _dp(a):

@@ -12,6 +12,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 BENCH = [2.0, 1.0, 1.0, 0.0, 1.0, 0.75, 0.0, 1.0, 1.0, 1.0]
 HARMONIC = [1.0, 2.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 1.0]
+GENERIC = [1.5, 2.0, 0.7, 0.3, 0.8, 0.6, 1.0, 0.5, 0.9, 0.7]
 
 
 def _mods():
@@ -29,7 +30,7 @@ def relerr(a, b):
 
 
 @pytest.mark.parametrize("variant", [0, 2, 3])
-@pytest.mark.parametrize("params", [BENCH, HARMONIC])
+@pytest.mark.parametrize("params", [BENCH, HARMONIC, GENERIC])
 def test_variant_parity(variant, params):
     P, C = _mods()
     n = (45, 22, 30)   # x not a multiple of the 32-point table tile
