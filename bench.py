@@ -31,8 +31,19 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
-BYTES_PER_POINT = {"wave": 432, "bssn": 2400}   # DESIGN.md §Roofline (one HBM pass per stage)
 METRIC = "grid-point updates/s per RK4 step (fp64)"
+
+# SURVEY.md §8(d) algorithmic accounting (one HBM pass per RK substep):
+#   wave: 432 B per point-update = stage 1..4: 64 + 136 + 112 + 120 B; the temporally blocked
+#         pair kernels carry stages 1+2 (200 B) and 3+4 (232 B) -- their own design moves only
+#         104 + 152 = 256 B (intermediate stages stay on chip), reported as the design figure;
+#   BSSN: 2400 B and ~22.7 k flops per point-update (App. A RHS ~5.6 k flops x 4 stages +
+#         the RK combinations), 1/4 of each per stage launch.
+WAVE_STAGE_BYTES = (64, 136, 112, 120)
+WAVE_PAIR_BYTES = (200, 232)
+WAVE_PAIR_DESIGN_BYTES = (104, 152)
+BSSN_BYTES = 2400
+BSSN_FLOPS = 22.7e3
 
 
 def measured_peaks():
@@ -40,39 +51,32 @@ def measured_peaks():
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic_table():
-    p = os.path.join(HERE, "profiles", "r1_traffic.json")
+def fp64_peaks():
+    """(derived, measured) fp64 peaks in TFLOP/s: derived = 148 SMs x 64 DFMA lanes x 2 flops x
+    the max SM clock (the guide's unit counts); measured = the committed DFMA
+    microbenchmark on this pool (scripts/fp64_peak.cu -> profiles/r2_fp64_peak.json)."""
+    derived = 148 * 64 * 2 * 1.965e9 / 1e12
+    meas = None
+    p = os.path.join(HERE, "profiles", "r2_fp64_peak.json")
     if os.path.exists(p):
         with open(p) as fh:
-            return json.load(fh)
-    return {}
+            d = json.load(fh)
+        meas = {"burst": d.get("burst_tflops"), "sustained": d.get("sustained_tflops")}
+    return derived, meas
 
 
-def measured_traffic(config: str, variant: int):
-    """DRAM bytes per step from the committed ncu capture of this config/variant (or None)."""
-    t = _traffic_table().get(config, {}).get(str(variant))
-    return None if t is None else t.get("dram_bytes_per_step")
-
-
-def bssn_fp64_roofline(pts: int, step_s: float, variant: int):
-    """fp64-pipe roofline for the BSSN step: thread-level fp64 instructions per point-update
-    of this kernel design (ncu sm__inst_executed_pipe_fp64 x 32 / points, committed in
-    profiles/r1_traffic.json) vs 148 SMs x 64 fp64 lanes x the max SM clock."""
-    tab = _traffic_table().get("bssn192", {})
-    t = tab.get(str(variant), {}).get("fp64_thread_instr_per_point_step") or \
-        tab.get("fp64_thread_instr_per_point_step")
-    if not t:
-        return {}
-    peak_inst = 148 * 64 * 1.965e9  # fp64 thread-instructions / s at max clock (DFMA = 2 flops)
-    achieved = t * pts / step_s
-    return {"bound": "alu", "pipe": "fp64", "achieved": achieved / 1e12, "peak": peak_inst / 1e12,
-            "unit": "T fp64 thread-instr/s", "frac": achieved / peak_inst,
-            "fp64_instr_per_point_step": t,
-            "hbm_frac_at_2400_bytes": 2400 * pts / step_s / 1e9 / measured_peaks()[0]}
+def committed_traffic(config: str, kernel: str):
+    """ncu dram__bytes_read+write per launch of `kernel` from the committed --set full capture
+    (profiles/r2_traffic.json), or None."""
+    p = os.path.join(HERE, "profiles", "r2_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh).get(config, {}).get(kernel)
 
 
 class ClockSampler:
@@ -219,6 +223,43 @@ def workload(args):
     raise SystemExit(f"unknown config {args.config}")
 
 
+def config0_report(P, C):
+    """configs[0]: wave 32^3, 4th-order FD, 3 ghosts, RK4, 10 steps.
+    The CPU oracle's wall time on 1 core and on all cores (each in a fresh subprocess, so
+    OMP_NUM_THREADS takes effect), and the GPU's parity against it on the same seeded input."""
+    import torch
+    import chemora_inputs as ci
+    import oracle
+    n = (32, 32, 32)
+    h = (2 * math.pi / 32,) * 3
+    dt = 0.25 * h[0]
+    code = ("import sys,time,math; sys.path.insert(0, %r); import chemora_inputs as ci, oracle; "
+            "n=(32,32,32); h=(2*math.pi/32,)*3; y=ci.pw3(n,h); oracle.rk4(1,y,h,0.25*h[0],1); "
+            "t=time.perf_counter(); oracle.rk4(1,y,h,0.25*h[0],10); print(time.perf_counter()-t)") % HERE
+    allc = len(os.sched_getaffinity(0))
+    secs = {}
+    for label, threads in (("1_core", 1), ("all_cores", allc)):
+        env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        secs[label] = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
+    y0 = ci.pw3(n, h)
+    ref = oracle.rk4(oracle.WAVE, y0, h, dt, 10)
+    g = P.Grid(C.SYS_WAVE, n, h, device=torch.cuda.current_device())
+    g.set_initial(C.INIT_HOST, y0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.rk4_step(dt, 10)
+    e1.record()
+    got = g.get_state()
+    err = max(float(np.abs(got[f] - ref[f]).max() / np.abs(ref[f]).max()) for f in range(5))
+    gms = e0.elapsed_time(e1)
+    g.close()
+    return {"workload": "configs[0]: scalar wave eq, 4th-order FD, 32^3 periodic, 3 ghost zones, RK4, 10 steps",
+            "oracle_seconds_1_core": secs["1_core"], "oracle_seconds_all_cores": secs["all_cores"],
+            "nproc": os.cpu_count(), "affinity_cores": allc, "omp_num_threads_all": allc,
+            "gpu_ms_10_steps": gms, "gpu_vs_oracle_max_rel_err": err, "tolerance": 1e-12}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -227,6 +268,8 @@ def main():
     ap.add_argument("--impl", default="chemora", choices=["chemora", "reference"])
     ap.add_argument("--config", default="wave512", choices=["wave512", "bssn192", "wave1024", "bssn384"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the BSSN 192^3 secondary line and the configs[0] report")
     # e2e steps: enough that the pipeline fill (first upload) and drain (last download) are
     # amortised -- per step the two PCIe directions then overlap (scripts/pcie_probe.py)
     ap.add_argument("--e2e-steps", type=int, default=12)
@@ -268,118 +311,151 @@ def main():
         watchdog = threading.Timer(float(os.environ.get("CHEMORA_BENCH_DEADLINE", "900")), _abort)
         watchdog.daemon = True
         watchdog.start()
-    cfg = workload(args)
-    n = cfg["n"]
-    system = C.SYS_WAVE if cfg["system"] == "wave" else C.SYS_BSSN
-    strong = cfg.get("strong", False)
-    if strong and (world < 2 or n[2] % world):
-        raise SystemExit(f"{args.config} is a strong-scaling config for 2/4/8 GPUs (z divisible by N)")
-    # weak scaling: n per GPU, the global z extent grows with N; strong: n is the global grid
-    gext = (n[0], n[1], n[2]) if strong else (n[0], n[1], n[2] * world)
-    L = 2 * math.pi if system == C.SYS_WAVE else 1.0
-    h = (L / n[0], L / n[1], L / n[2])
-    dt = 0.25 * min(h)
-    order = args.fd_order if system == C.SYS_WAVE else 4
-    ghost = max(3, order // 2)
-    if order != 4:
-        cfg["config"] = dict(cfg["config"], fd_order=order, ghost=ghost)
-    g = P.Grid(system, gext, h, device=local, rank=rank, nranks=world, ghost=ghost, fd_order=order)
-    if args.variant is not None:
-        g.set_kernel_variant(args.variant)
-    if world > 1:
-        g.connect_ipc(host_barrier=shared)
-    init = C.INIT_PLANE_WAVES if system == C.SYS_WAVE else C.INIT_MINK_PERT
-    g.set_initial(init, seed=1410)
-    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        g.rk4_step(dt, 1)
-    barrier()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(local) as clk:
-        barrier()
-        ev[0].record(stream)
-        for s in range(args.steps):
-            g.rk4_step(dt, 1)
-            ev[s + 1].record(stream)
-        barrier()
-    step_ms = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
-    if world > 1:
-        t = torch.tensor([total_ms], device="cpu" if shared else "cuda")
+    def allmax(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    pts_local = n[0] * n[1] * (n[2] // world if strong else n[2])
-    value = pts_local * world * args.steps / (total_ms * 1e-3)
+        return float(t.item())
 
-    # roofline of the dominant kernel(s): the kernels of one RK4 step are the only launches in
-    # the timed region.  Algorithmic bytes are those of the active kernel design: 432 B/pt for
-    # one kernel per RK stage, 256 B/pt for the temporally blocked stage
-    # pairs -- the frac is against that design's own HBM floor.
-    peak, peak_kind = measured_peaks()
-    mean_step_s = float(np.mean(step_ms)) * 1e-3
-    variant = g.kernel_variant()
-    floor_bpp = BYTES_PER_POINT[cfg["system"]]
-    pair_kernels = cfg["system"] == "wave" and variant in (6, 7, 8)   # temporally blocked pairs
-    bpp = 256 if pair_kernels else floor_bpp
-    achieved = bpp * pts_local / mean_step_s / 1e9
-    traffic = measured_traffic(args.config, variant) if order == 4 else None
-    kname = ({6: "wave_fused<A>, wave_fused<B>", 7: "wave_fused2<A>, wave_fused2<B>",
-              8: "wave_fused3<A>, wave_fused3<B>"}.get(variant, "") + " (2 launches = 1 step)" if bpp == 256 else
-             "stage kernels (4 launches x groups = 1 step)")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                "kernel": kname, "variant": variant,
-                "algorithmic_bytes_per_point": bpp,
-                "traffic_note": "ncu dram__bytes_read+write per step (all launches of one step), profiles/r1_traffic.json",
-                "one_pass_per_stage_bytes_per_point": floor_bpp,
-                "frac_at_one_pass_per_stage_bytes": floor_bpp * pts_local / mean_step_s / 1e9 / peak,
-                "frac_of_nominal_8TBps": achieved / 8000.0}
-    # our kernel launches per RK4 step: wave 2 (stage pairs) or 4 (one per stage); BSSN
-    # 4 (two-phase table kernel, variant 0, or fused single kernel, 1) or 3 fissioned
-    # groups x 4 stages (variant 2), or derivative + 2 algebra kernels x 4 stages (variant 3)
-    if cfg["system"] == "wave":
-        launches_per_step = 2 if pair_kernels else 4
-    else:
-        launches_per_step = 12 if variant in (2, 3) else 4
-    if cfg["system"] == "bssn":
-        # BSSN is bound by the fp64 pipe: fp64 instructions per point-update
-        # counted by ncu (profiles/r1_traffic.json) against 64 DFMA lanes/SM/clock.
-        roofline.update(bssn_fp64_roofline(pts_local, mean_step_s, variant))
+    def measure(config, steps, warmup, e2e_steps):
+        a2 = argparse.Namespace(**vars(args))
+        a2.config = config
+        cfg = workload(a2)
+        n = cfg["n"]
+        system = C.SYS_WAVE if cfg["system"] == "wave" else C.SYS_BSSN
+        strong = cfg.get("strong", False)
+        if strong and (world < 2 or n[2] % world):
+            raise SystemExit(f"{config} is a strong-scaling config for 2/4/8 GPUs (z divisible by N)")
+        # weak scaling: n per GPU, the global z extent grows with N; strong: n is the global grid
+        gext = (n[0], n[1], n[2]) if strong else (n[0], n[1], n[2] * world)
+        L = 2 * math.pi if system == C.SYS_WAVE else 1.0
+        h = (L / n[0], L / n[1], L / n[2])
+        dt = 0.25 * min(h)
+        order = args.fd_order if system == C.SYS_WAVE else 4
+        ghost = max(3, order // 2)
+        if order != 4:
+            cfg["config"] = dict(cfg["config"], fd_order=order, ghost=ghost)
 
-    # e2e through the public API with host buffers: per step, upload the state from pinned
-    # host memory, one RK4 step, download the state.  On one GPU two grid handles alternate on
-    # two streams (chemora_upload_state / chemora_download_state are stream-ordered), so one
-    # step's download overlaps the next step's upload on the two copy engines; every step
-    # still moves its full input and output through PCIe inside the timed region.
-    e2e = None
-    if args.e2e_steps > 0:
+        def make_grid():
+            gg = P.Grid(system, gext, h, device=local, rank=rank, nranks=world, ghost=ghost, fd_order=order)
+            if args.variant is not None:
+                gg.set_kernel_variant(args.variant)
+            return gg
+        g = make_grid()
+        if world > 1:
+            g.connect_ipc(host_barrier=shared)
+        init = C.INIT_PLANE_WAVES if system == C.SYS_WAVE else C.INIT_MINK_PERT
+        g.set_initial(init, seed=1410)
+        stream = torch.cuda.current_stream()
+        for _ in range(warmup):
+            g.rk4_step(dt, 1)
+        barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        C.chemora_set_launch_timing(g.handle, True)
+        with ClockSampler(local) as clk:
+            barrier()
+            ev[0].record(stream)
+            for s in range(steps):
+                g.rk4_step(dt, 1)
+                ev[s + 1].record(stream)
+            barrier()
+        ms_sum, counts = C.chemora_read_launch_timing(g.handle, g.stream)
+        C.chemora_set_launch_timing(g.handle, False)
+        step_ms = [ev[s].elapsed_time(ev[s + 1]) for s in range(steps)]
+        total_ms = allmax(ev[0].elapsed_time(ev[-1]))
+        pts_local = n[0] * n[1] * (n[2] // world if strong else n[2])
+        value = pts_local * world * steps / (total_ms * 1e-3)
+        mean_step_s = total_ms * 1e-3 / steps
+        variant = g.kernel_variant()
+
+        # roofline of the dominant launch (the slot with the largest share of the step), its
+        # average duration from the CUDA events the library recorded around every launch on
+        # the launching stream during the timed region
+        slots = [s for s in range(8) if counts[s] > 0]
+        avg = {s: ms_sum[s] / counts[s] for s in slots}
+        dom = max(slots, key=lambda s: ms_sum[s])
+        share = ms_sum[dom] / max(sum(ms_sum[s] for s in slots), 1e-30)
+        if system == C.SYS_WAVE:
+            peak, peak_src = measured_peaks()
+            pair = len(slots) == 2
+            per_slot = WAVE_PAIR_BYTES if pair else WAVE_STAGE_BYTES
+            kname = ("wave_fused3<%s> (stages %s)" % ("AB"[dom], "1+2" if dom == 0 else "3+4")) if pair \
+                else f"wave stage-{dom + 1} kernel (variant {variant})"
+            achieved = per_slot[dom] * pts_local / (avg[dom] * 1e-3) / 1e9
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": committed_traffic(config, kname.split(" ")[0]),
+                        "peak_source": peak_src, "kernel": kname, "variant": variant,
+                        "alg_bytes_per_point_per_launch": per_slot[dom],
+                        "alg_bytes_note": "SURVEY.md §8(d): 432 B/pt per RK4 step = stages 64+136+112+120",
+                        "launch_ms_avg": avg[dom], "launch_share_of_step": share,
+                        "step_frac_at_432_bytes": 432 * pts_local / mean_step_s / 1e9 / peak,
+                        "frac_of_nominal_8TBps": achieved / 8000.0}
+            if pair:
+                d = WAVE_PAIR_DESIGN_BYTES[dom]
+                roofline["design_bytes_per_point_per_launch"] = d
+                roofline["frac_at_design_bytes"] = d * pts_local / (avg[dom] * 1e-3) / 1e9 / peak
+        else:
+            derived, meas = fp64_peaks()
+            flops = BSSN_FLOPS / 4 * pts_local
+            achieved = flops / (avg[dom] * 1e-3) / 1e12
+            roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": derived, "unit": "TFLOP/s",
+                        "frac": achieved / derived, "traffic": committed_traffic(config, f"bssn_stage{dom + 1}"),
+                        "peak_source": "derived: 148 SMs x 64 DFMA lanes x 2 flops x 1.965 GHz (DESIGN.md §7)",
+                        "kernel": f"BSSN RK stage {dom + 1} (variant {variant})", "variant": variant,
+                        "alg_flops_per_point_per_launch": BSSN_FLOPS / 4,
+                        "alg_flops_note": "SURVEY.md §8(d): ~22.7 k flops per point-update (FMA = 2)",
+                        "launch_ms_avg": avg[dom], "launch_share_of_step": share,
+                        "hbm_frac_at_2400_bytes": BSSN_BYTES * pts_local / mean_step_s / 1e9 / measured_peaks()[0]}
+            if meas and meas.get("sustained"):
+                roofline["peak_measured_sustained"] = meas["sustained"]
+                roofline["peak_measured_burst"] = meas["burst"]
+                roofline["frac_of_measured_sustained"] = achieved / meas["sustained"]
+        per_slot_ms = {f"slot{s}": {"avg_ms": avg[s], "launches": counts[s]} for s in slots}
+        kernels_per_slot = 3 if (system == C.SYS_BSSN and variant in (2, 3)) else 1
+        launches = kernels_per_slot * sum(counts[s] for s in slots)
+
+        e2e = None
+        if e2e_steps > 0:
+            e2e = run_e2e(g, make_grid, dt, e2e_steps, pts_local)
+        cfgout = dict(cfg["config"])
+        cfgout["parallelism"] = f"z-slab x{world}" if world > 1 else "single GPU"
+        cfgout["global_grid"] = list(gext)
+        line = {"metric": METRIC, "value": value, "unit": "grid-point updates/s", "n_gpus": world,
+                "steps": steps, "warmup": warmup, "ms_per_step": total_ms / steps,
+                "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": cfgout, "roofline": roofline,
+                "e2e": e2e, "gpu_launches": launches, "launch_timing": per_slot_ms,
+                "clocks": clk.summary(), "step_ms": step_ms}
+        g.close()
+        return line, cfg
+
+    def run_e2e(g, make_grid, dt, e2e_steps, pts_local):
+        # e2e through the public API with host buffers: per step, upload the state from pinned
+        # host memory, one RK4 step, download the state.  On one GPU up to three grid handles
+        # take turns on their own streams, so one handle's upload, another's step and a
+        # third's download overlap (H2D engine, SMs, D2H engine); every step still moves its
+        # whole input and output over PCIe inside the timed region
+        import psutil
+        stream = torch.cuda.current_stream()
         shape = g.interior_shape()
         nbytes = int(np.prod(shape)) * 8
-        # on one GPU up to three grid handles take turns on their own streams, so one
-        # handle's upload, another's step and a third's download overlap (H2D engine, SMs,
-        # D2H engine); each step still moves its whole input and output over PCIe
-        # pinned host buffers: 2 per handle per rank on this node, kept under half the RAM
-        import psutil
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
         max_nb = int(0.5 * psutil.virtual_memory().available // (2 * nbytes * local_world))
-        grids = [g]
-        while (world == 1 and len(grids) < min(3, max_nb)
-               and torch.cuda.mem_get_info()[0] > g.nbytes + (2 << 30)):
-            g2 = P.Grid(system, gext, h, device=local, rank=rank, nranks=world, ghost=ghost, fd_order=order)
-            if args.variant is not None:
-                g2.set_kernel_variant(args.variant)
-            grids.append(g2)
-        nb = len(grids)
-        pipelined = nb > 1
         if max_nb < 1:
             raise SystemExit(f"e2e: {2 * nbytes * local_world / 2**30:.0f} GiB of pinned host buffers "
                              f"do not fit this node's RAM; rerun with --e2e-steps 0")
+        grids = [g]
+        while (world == 1 and len(grids) < min(3, max_nb)
+               and torch.cuda.mem_get_info()[0] > g.nbytes + (2 << 30)):
+            grids.append(make_grid())
+        nb = len(grids)
         host_in = [torch.empty(shape, dtype=torch.float64, pin_memory=True) for _ in range(nb)]
         host_out = [torch.empty(shape, dtype=torch.float64, pin_memory=True) for _ in range(nb)]
         g.get_state(out=host_in[0].numpy())
@@ -391,7 +467,7 @@ def main():
         e0.record(stream)
         for s in streams:
             s.wait_event(e0)
-        for it in range(args.e2e_steps):
+        for it in range(e2e_steps):
             b = it % nb
             with torch.cuda.stream(streams[b]):
                 grids[b].upload_state(host_in[b])
@@ -401,31 +477,30 @@ def main():
             stream.wait_stream(s)
         e1.record(stream)
         barrier()
-        e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([e_ms], device="cpu" if shared else "cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": pts_local * world * args.e2e_steps / (e_ms * 1e-3), "unit": "grid-point updates/s",
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
-               "what": ("chemora_upload_state (pinned) + chemora_rk4_step(1) + chemora_download_state per "
-                        "step" + (f", {nb} grid handles taking turns on {nb} streams" if pipelined else ""))}
+        e_ms = allmax(e0.elapsed_time(e1))
         for gg in grids[1:]:
             gg.close()
+        return {"value": pts_local * world * e2e_steps / (e_ms * 1e-3), "unit": "grid-point updates/s",
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": e2e_steps,
+                "what": ("chemora_upload_state (pinned) + chemora_rk4_step(1) + chemora_download_state per step"
+                         + (f", {nb} grid handles taking turns on {nb} streams" if nb > 1 else ""))}
 
+    line, cfg = measure(args.config, args.steps, args.warmup, args.e2e_steps)
+    secondary = {}
+    if args.config == "wave512" and args.fd_order == 4 and args.variant is None and not args.no_secondary:
+        # BSSN 192^3 per GPU (configs[2]) timed in the same run, under its own key
+        sl, _ = measure("bssn192", max(5, args.steps // 3), args.warmup, 0)
+        secondary["bssn192"] = {k: sl[k] for k in ("value", "unit", "ms_per_step", "steps", "warmup", "config",
+                                                     "roofline", "gpu_launches", "launch_timing", "clocks")}
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu_baseline:
             cb = oracle_sample(cfg["system"], 15.0)[0]
-        cfgout = dict(cfg["config"])
-        cfgout["parallelism"] = f"z-slab x{world}" if world > 1 else "single GPU"
-        cfgout["global_grid"] = list(gext)
-        line = {"metric": METRIC, "value": value, "unit": "grid-point updates/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-                "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": cfgout, "roofline": roofline, "cpu_baseline": cb,
-                "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
-                "step_ms": step_ms}
+        line["cpu_baseline"] = cb
+        if secondary:
+            line["secondary"] = secondary
+        if world == 1 and args.config == "wave512" and not args.no_secondary:
+            line["config0"] = config0_report(P, C)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -281,6 +281,18 @@ int chemora_constraint_norms_combine(const chemora_grid_desc* desc, const double
 int chemora_autotune(chemora_grid_t grid, int32_t trials, int32_t* chosen, double* ms_out,
                      void* stream);
 
+/* ---- measurement */
+
+/* Per-launch timing of the step (for roofline reporting): while enabled, every kernel launch
+ * of chemora_rk4_step is bracketed by CUDA events recorded on the launching stream (up to
+ * 4096 launches between reads).  chemora_read_launch_timing synchronises the stream and
+ * returns, per launch slot s < 8 (wave temporally blocked path: 0 = stage pair 1+2, 1 =
+ * stage pair 3+4; otherwise RK stage s+1), the summed milliseconds ms_sum[s] and the number
+ * of launches counts[s] since the last read (both arrays of 8), then clears them.  Enabling
+ * resets the record. */
+int chemora_set_launch_timing(chemora_grid_t grid, int enable);
+int chemora_read_launch_timing(chemora_grid_t grid, double* ms_sum, int32_t* counts, void* stream);
+
 /* ---- testing hooks (not part of the user-facing contract) */
 
 /* Select the kernel design of this handle.  WAVE: 0 = one thread per point,

@@ -83,6 +83,8 @@ _SIGS = {
     "chemora_read_monitor_multi": ([ctypes.POINTER(_vp), ctypes.c_int32, _dp, ctypes.c_int32,
                                     ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
     "chemora_set_phase_barrier": ([_vp, _vp, _vp], ctypes.c_int),
+    "chemora_set_launch_timing": ([_vp, ctypes.c_int], ctypes.c_int),
+    "chemora_read_launch_timing": ([_vp, _dp, ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
     "chemora_constraint_norms_combine": ([_descp, _dp, ctypes.c_int32, _dp], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -294,6 +296,18 @@ def chemora_read_monitor_multi(handles, max_steps: int = 1024, stream=None) -> n
     _check(_lib.chemora_read_monitor_multi(arr, len(handles), _dptr(out), max_steps, ctypes.byref(cnt), stream),
            "chemora_read_monitor_multi")
     return out[:cnt.value].copy()
+
+
+def chemora_set_launch_timing(h, enable: bool):
+    _check(_lib.chemora_set_launch_timing(h, 1 if enable else 0), "chemora_set_launch_timing")
+
+
+def chemora_read_launch_timing(h, stream=None):
+    """-> (ms_sum[8], counts[8]) per launch slot since the last read."""
+    ms = np.zeros(8)
+    cnt = (ctypes.c_int32 * 8)()
+    _check(_lib.chemora_read_launch_timing(h, _dptr(ms), cnt, stream), "chemora_read_launch_timing")
+    return ms, list(cnt)
 
 
 BARRIER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)

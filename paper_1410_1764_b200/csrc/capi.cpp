@@ -84,6 +84,11 @@ struct chemora_grid_s {
   double* lo_gather;            // the lower neighbour's gather buffer (IPC mapping)
   void (*barrier_fn)(void*);    // optional host barrier after every phase (shared device)
   void* barrier_user;
+  // per-launch timing (chemora_set_launch_timing): events around every step launch
+  bool timing;
+  std::vector<cudaEvent_t> tev;  // pairs (begin, end)
+  std::vector<int> tslot;        // launch slot of each pair
+  size_t tn;                     // pairs recorded since the last read
 };
 
 namespace {
@@ -321,6 +326,32 @@ int ring_allgather(chemora_grid_t g, const double* host_src, int len, double* ho
   return CHEMORA_OK;
 }
 
+// Launch timing: CUDA events recorded on the launching stream around each kernel launch of
+// a step (slot = which launch of the step: wave pair A/B = 0/1, else RK stage 1..4 = 0..3).
+constexpr size_t kMaxTimed = 4096;
+constexpr int kTimingSlots = 8;
+cudaError_t tmark(chemora_grid_t g, int slot, bool begin, cudaStream_t st) {
+  if (!g->timing) return cudaSuccess;
+  if (begin) {
+    if (g->tn >= kMaxTimed) return cudaSuccess;  // full: later launches are not timed
+    if (g->tev.size() < 2 * (g->tn + 1)) {
+      for (int q = 0; q < 2; ++q) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r != cudaSuccess) return r;
+        g->tev.push_back(e);
+      }
+    }
+    if (g->tslot.size() < g->tn + 1) g->tslot.resize(g->tn + 1);
+    g->tslot[g->tn] = slot;
+    return cudaEventRecord(g->tev[2 * g->tn], st);
+  }
+  if (g->tn >= kMaxTimed) return cudaSuccess;
+  cudaError_t r = cudaEventRecord(g->tev[2 * g->tn + 1], st);
+  g->tn += 1;
+  return r;
+}
+
 StageLaunch stage_args(chemora_grid_t g, double dt) {
   StageLaunch a;
   a.L = g->L;
@@ -468,6 +499,8 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->lo_gather = nullptr;
   g->barrier_fn = nullptr;
   g->barrier_user = nullptr;
+  g->timing = false;
+  g->tn = 0;
   auto* fl = reinterpret_cast<unsigned long long*>(g->ws + P.flags);
   g->nan_flag = fl;
   g->flags = fl + 1;
@@ -511,6 +544,7 @@ int chemora_grid_destroy(chemora_grid_t g) {
   {
     DeviceGuard dg(g->desc.device);
     for (void* p : g->opened) cudaIpcCloseMemHandle(p);
+    for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
   }
   delete g;
   return CHEMORA_OK;
@@ -707,7 +741,9 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
           CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
           a.mon_partials = g->mon_partials;
         }
+        CUDA_TRY(tmark(g, pair, true, st));
         CUDA_TRY(fused_pair(g->variant, a, pair, st));
+        CUDA_TRY(tmark(g, pair, false, st));
         if (pair == 1 && mon) {
           CUDA_TRY(monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st));
           g->mon_written += 1;
@@ -727,7 +763,9 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
         CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
         a.mon_partials = g->mon_partials;
       }
+      CUDA_TRY(tmark(g, s - 1, true, st));
       CUDA_TRY(launch_stage(g, a, s, st));
+      CUDA_TRY(tmark(g, s - 1, false, st));
       if (s == 4 && mon) {
         CUDA_TRY(monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st));
         g->mon_written += 1;
@@ -900,6 +938,29 @@ int chemora_read_monitor_multi(chemora_grid_t* grids, int32_t n, double* out, in
   }
   *count = cnt0;
   return status;
+}
+
+int chemora_set_launch_timing(chemora_grid_t g, int enable) {
+  if (int rc = check_grid(g)) return rc;
+  g->timing = enable != 0;
+  g->tn = 0;
+  return CHEMORA_OK;
+}
+
+int chemora_read_launch_timing(chemora_grid_t g, double* ms_sum, int32_t* counts, void* stream) {
+  if (int rc = check_grid(g)) return rc;
+  if (!ms_sum || !counts) return fail(CHEMORA_E_INVALID, "output is NULL");
+  DeviceGuard dg(g->desc.device);
+  CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  for (int s = 0; s < kTimingSlots; ++s) { ms_sum[s] = 0.0; counts[s] = 0; }
+  for (size_t i = 0; i < g->tn; ++i) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, g->tev[2 * i], g->tev[2 * i + 1]));
+    const int s = g->tslot[i];
+    if (s >= 0 && s < kTimingSlots) { ms_sum[s] += ms; counts[s] += 1; }
+  }
+  g->tn = 0;
+  return CHEMORA_OK;
 }
 
 int chemora_set_phase_barrier(chemora_grid_t g, void (*fn)(void*), void* user) {
