@@ -20,7 +20,8 @@ NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-rela
 # the wave kernels exist in two tilings that must agree bitwise: no implicit FMA
 # contraction there (every fma is explicit in the source)
 NO_FMAD = {"wave_stage.cu", "wave_tma.cu", "wave_fused3.cu"}
-SOURCES = ["wave_stage.cu", "wave_tma.cu", "wave_fused3.cu", "bssn_stage.cu", "ghost_init_norms.cu", "capi.cpp"]
+SOURCES = ["wave_stage.cu", "wave_tma.cu", "wave_fused3.cu", "bssn_stage.cu", "bssn_fused.cu", "ghost_init_norms.cu",
+           "capi.cpp"]
 
 
 def _deps():

@@ -1,0 +1,357 @@
+// bssn_fused.cu -- BSSN kernel variant 4 (default): ONE fused kernel per RK stage, the
+// derivatives computed on chip where the algebra needs them -- no derivative table in HBM.
+//
+// The paper's Einstein kernels are "too large in data and instructions" and need fission
+// (PAPER.md:537-547, 699-700); on B200 the round-1 fission went through an HBM table of 136
+// derivative slots per point (5.8x the algorithmic DRAM traffic).  Here the data that makes
+// the fused kernel too large is split across the SM's three on-chip stores instead:
+//
+//   * shared memory holds the current z-plane of ALL 25 GFs on a 16x8 tile with a 3-point
+//     halo (TMA 4-D box (22, 14, 1, 25), double-buffered so the next plane streams in while
+//     this one is used): every x and y stencil (D1, D2, upwind, mixed xy) reads it;
+//   * TENSOR MEMORY holds each point's own z-column window, planes k-3 .. k+3 of all 25 GFs
+//     (TMEM lane = point, 16 columns per GF; 400 of the 512 columns), shifted by one plane per
+//     step: the z stencils (D1, D2, upwind) read it with one tcgen05.ld per GF;
+//   * small shared helper planes hold the inner derivatives of the mixed stencils (D1_y on
+//     the x-extended tile for d_x d_y, D1_z on the x- and y-extended tile for d_x d_z and
+//     d_y d_z; the tile interior from the TMEM windows, the 2-point frame from L2).
+//
+// The CTA (one per SM, persistent over (tile, z-chunk) items) has 256 threads: every point
+// of the tile is served by two threads in warps w and w+4, which share the TMEM lanes of the
+// point -- one runs the curvature group G2 (trK, At, A), the other the kinematic + shift
+// group G13 (phi, gt, alpha, beta, Xt, B) of bssn_point, each followed by its RK4 update.
+// HBM traffic is the one-pass-per-stage floor plus L2-resident halo re-reads.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "bssn_common.cuh"
+#include "tma.cuh"
+
+namespace chemora {
+namespace {
+
+constexpr int FX = 16, FY = 8, FPT = FX * FY;          // tile points = TMEM lanes used
+constexpr int FR = 3;                                  // halo (upwind radius)
+constexpr int FSX = FX + 2 * FR, FSY = FY + 2 * FR, FPL = FSX * FSY;   // 22 x 14
+constexpr int FNT = 2 * FPT;                           // (point, group) threads
+constexpr int NMIX = 11;                               // GFs with mixed second derivatives
+constexpr int HXW = FX + 4;                            // x-extended helper rows: i = -2 .. FX+1
+constexpr int HYH = FY + 4;                            // y-extended helper columns: j = -2 .. FY+1
+constexpr int TILE_BYTES = NV * FPL * 8;               // one plane of all GFs (61600 B)
+constexpr int TILE_STRIDE = (TILE_BYTES + 1023) / 1024 * 1024;
+constexpr int GZX_N = NMIX * FY * HXW, GZY_N = NMIX * HYH * FX, GYX_N = NMIX * FY * HXW;
+constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64;
+constexpr int FEED0 = 13;                              // group 0 feeds GFs [0, 13), group 1 [13, 25)
+constexpr int NFRAME = 2 * 2 * FY + 2 * 2 * FX;        // 2-point x- and y-frames of the tile: 96
+
+// ---- TMEM (tcgen05) helpers: each thread reads / writes its own lane
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta)
+      : "memory");
+}
+__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ double dbl(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
+__device__ __forceinline__ void cta_sync_tm() {
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+}
+
+// z-window of GF gf: planes k-3 .. k+3 (slots 0..6) of the thread's point
+struct ZWin {
+  double w[7];
+};
+__device__ __forceinline__ ZWin zwin(uint32_t tb, int gf) {
+  uint32_t r[16];
+  tm_ld16(tb + 16u * (uint32_t)gf, r);
+  tm_wait_ld();
+  ZWin z;
+#pragma unroll
+  for (int s = 0; s < 7; ++s) z.w[s] = dbl(r[2 * s], r[2 * s + 1]);
+  return z;
+}
+
+// Derivative provider of the fused kernel (same operation order as StencilP: D1raw, D2raw,
+// D11raw with the outer sum along the first axis of the pair, ADVraw).
+struct FusedP {
+  const double* t;     // plane-k tile of all GFs, [gf][FSY][FSX]
+  int c;               // own point's offset in a GF plane of the tile
+  const double* gzx;   // [NMIX][FY][HXW]   D1raw_z, x-extended
+  const double* gzy;   // [NMIX][HYH][FX]   D1raw_z, y-extended
+  const double* gyx;   // [NMIX][FY][HXW]   D1raw_y, x-extended
+  int hx, hy;          // own point's offsets in the x- / y-extended helper planes
+  uint32_t tb;         // TMEM address of the point's lane, column 0
+  __device__ __forceinline__ double v(int gf) const { return t[gf * FPL + c]; }
+  __device__ __forceinline__ double d1(const BssnK& K, int gf, int l) const {
+    if (l == 2) {
+      const ZWin z = zwin(tb, gf);
+      return (8.0 * (z.w[4] - z.w[2]) - (z.w[5] - z.w[1])) * K.i12h[2];
+    }
+    const double* f = t + gf * FPL + c;
+    const int s = l == 0 ? 1 : FSX;
+    return (8.0 * (f[s] - f[-s]) - (f[2 * s] - f[-2 * s])) * K.i12h[l];
+  }
+  __device__ __forceinline__ double dd(const BssnK& K, int gf, int l, int m, double f0) const {
+    if (l == m) {
+      if (l == 2) {
+        const ZWin z = zwin(tb, gf);
+        return (16.0 * (z.w[4] + z.w[2]) - (z.w[5] + z.w[1]) - 30.0 * f0) * K.i12h2[2];
+      }
+      const double* f = t + gf * FPL + c;
+      const int s = l == 0 ? 1 : FSX;
+      return (16.0 * (f[s] + f[-s]) - (f[2 * s] + f[-2 * s]) - 30.0 * f0) * K.i12h2[l];
+    }
+    const int e = ddi(gf);
+    const double* g;
+    int s;
+    if (m == 1) { g = gyx + e * (FY * HXW) + hx; s = 1; }          // (x, y): outer x of D1_y
+    else if (l == 0) { g = gzx + e * (FY * HXW) + hx; s = 1; }     // (x, z): outer x of D1_z
+    else { g = gzy + e * (HYH * FX) + hy; s = FX; }                // (y, z): outer y of D1_z
+    return (8.0 * (g[s] - g[-s]) - (g[2 * s] - g[-2 * s])) * K.i144hh[l + m - 1];
+  }
+  __device__ __forceinline__ double adv(const BssnK& K, int gf, const double* beta, double f0) const {
+    const double* f = t + gf * FPL + c;
+    double r = 0.0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int s = a == 0 ? 1 : FSX;
+      const double a1 = f[s], b1 = f[-s], a2 = f[2 * s], b2 = f[-2 * s], a3 = f[3 * s], b3 = f[-3 * s];
+      const double S = 21.0 * (a1 - b1) - 6.0 * (a2 - b2) + (a3 - b3);
+      const double A = 15.0 * (a1 + b1) - 6.0 * (a2 + b2) + (a3 + b3) - 20.0 * f0;
+      r = fma(fma(beta[a], S, fabs(beta[a]) * A), K.i24h[a], r);
+    }
+    const ZWin z = zwin(tb, gf);
+    const double S = 21.0 * (z.w[4] - z.w[2]) - 6.0 * (z.w[5] - z.w[1]) + (z.w[6] - z.w[0]);
+    const double A = 15.0 * (z.w[4] + z.w[2]) - 6.0 * (z.w[5] + z.w[1]) + (z.w[6] + z.w[0]) - 20.0 * f0;
+    return fma(fma(beta[2], S, fabs(beta[2]) * A), K.i24h[2], r);
+  }
+};
+
+struct FusedMaps {
+  CUtensorMap in;  // the stage input set, box (FSX, FSY, 1, NV)
+};
+
+template <int STAGE>
+__global__ void __launch_bounds__(FNT, 1)
+    bssn_fused(const __grid_constant__ FusedMaps M, StageLaunch a, BssnK K, int ntx, int nty, int chunk,
+               int nitems, double* rhs_dst) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* tiles = reinterpret_cast<double*>(smem);                       // 2 x TILE_STRIDE bytes
+  double* gzx = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE);
+  double* gzy = gzx + GZX_N;
+  double* gyx = gzy + GZY_N;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(gyx + GYX_N);           // 2 mbarriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  const Layout& L = a.L;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = warp >> 2;                     // 0: G2, 1: G13
+  const int p = (warp & 3) * 32 + lane;          // point of the tile (= TMEM lane)
+  const int tx = p % FX, ty = p / FX;
+  const double* in = stage_input<STAGE>(a);
+  const int ntiles = ntx * nty;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+    prefetch_tmap(&M.in);
+  }
+  cta_sync_tm();
+  const uint32_t tb = *tmem_slot + ((uint32_t)((warp & 3) * 32) << 16);
+
+  // (item, plane) sequence of this CTA: items it = blockIdx.x + q * gridDim.x, chunk-major
+  auto item_geom = [&](int it, int& i0, int& j0, int& kb, int& ke) {
+    const int ch = it / ntiles, tile = it % ntiles;
+    i0 = (tile % ntx) * FX;
+    j0 = (tile / ntx) * FY;
+    kb = a.k_begin + ch * chunk;
+    ke = min(kb + chunk, a.k_end);
+  };
+  auto issue_tile = [&](int buf, int i0, int j0, int k) {
+    mbar_arrive_expect_tx(&mbar[buf], (uint32_t)TILE_BYTES);
+    tma_load_4d(tiles + (size_t)buf * (TILE_STRIDE / 8), &M.in, &mbar[buf], kXOff + i0 - FR, L.g + j0 - FR,
+                L.g + k, 0);
+  };
+  const int64_t gfs = L.gfs;
+  const int xlo = -L.g, xhi = (int)L.nx + L.g - 1, ylo = -L.g, yhi = (int)L.ny + L.g - 1;
+  uint32_t phase = 0;  // parity bit per tile buffer
+  int n = 0;           // planes processed by this CTA (buffer = n & 1)
+  if (tid == 0 && (int)blockIdx.x < nitems) {
+    int i0, j0, kb, ke;
+    item_geom(blockIdx.x, i0, j0, kb, ke);
+    issue_tile(0, i0, j0, kb);
+  }
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int i0, j0, kb, ke;
+    item_geom(it, i0, j0, kb, ke);
+    const int i = i0 + tx, j = j0 + ty;
+    const bool live = i < L.nx && j < L.ny;
+    const int ic = min(i, (int)L.nx - 1), jc = min(j, (int)L.ny - 1);  // dead lanes: a valid column
+    const double* col = in + (int64_t)jc * L.px + ic;                   // own column, plane 0, GF 0
+    const int g_lo = grp == 0 ? 0 : FEED0, g_hi = grp == 0 ? FEED0 : NV;
+    // ---- window fill: planes kb-4 .. kb+2 into slots 0..6 (slot 0 is dropped by the first shift)
+    for (int gf = g_lo; gf < g_hi; ++gf) {
+      uint32_t r[16];
+#pragma unroll
+      for (int s = 0; s < 7; ++s) {
+        const int kk = max(kb - 4 + s, -L.g);
+        const double v = __ldg(col + gf * gfs + (int64_t)kk * L.plane);
+        r[2 * s] = (uint32_t)__double2loint(v);
+        r[2 * s + 1] = (uint32_t)__double2hiint(v);
+      }
+      r[14] = r[15] = 0u;
+      tm_st16(tb + 16u * (uint32_t)gf, r);
+    }
+    tm_wait_st();
+    for (int k = kb; k < ke; ++k, ++n) {
+      const int buf = n & 1;
+      // ---- next plane's tile (this item's k+1, or the next item's first plane) into the other
+      // buffer: its last reader (plane n-1) finished at the end-of-plane barrier
+      if (tid == 0) {
+        if (k + 1 < ke) issue_tile(buf ^ 1, i0, j0, k + 1);
+        else if (it + (int)gridDim.x < nitems) {
+          int ni0, nj0, nkb, nke;
+          item_geom(it + gridDim.x, ni0, nj0, nkb, nke);
+          issue_tile(buf ^ 1, ni0, nj0, nkb);
+        }
+      }
+      // ---- own-column values of plane k+3 for this thread's GF half (consumed by the shift)
+      double feed[NV - FEED0 > FEED0 ? NV - FEED0 : FEED0];
+#pragma unroll
+      for (int q = 0; q < FEED0; ++q) {
+        const int gf = g_lo + q;
+        if (gf < g_hi) feed[q] = __ldg(col + gf * gfs + (int64_t)(k + 3) * L.plane);
+      }
+      mbar_wait(&mbar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      const double* t = tiles + (size_t)buf * (TILE_STRIDE / 8);
+      // ---- helper: D1raw_y on the x-extended tile (inner derivative of d_x d_y), from the tile
+      for (int q = tid; q < GYX_N; q += FNT) {
+        const int e = q / (FY * HXW), rem = q % (FY * HXW);
+        const int jj = rem / HXW, ii = rem % HXW - 2;
+        const double* f = t + ddgf(e) * FPL + (jj + FR) * FSX + (ii + FR);
+        gyx[q] = 8.0 * (f[FSX] - f[-FSX]) - (f[2 * FSX] - f[-2 * FSX]);
+      }
+      // ---- helper: D1raw_z on the 2-point frame around the tile (from L2)
+      for (int q = tid; q < NMIX * NFRAME; q += FNT) {
+        const int e = q / NFRAME, f = q % NFRAME;
+        int ii, jj;
+        if (f < 4 * FY) { jj = f >> 2; const int cc = f & 3; ii = cc < 2 ? cc - 2 : FX + cc - 2; }
+        else { const int f2 = f - 4 * FY; ii = f2 % FX; const int rr = f2 / FX; jj = rr < 2 ? rr - 2 : FY + rr - 2; }
+        const int gx = min(max(i0 + ii, xlo), xhi), gy = min(max(j0 + jj, ylo), yhi);
+        const double* src = in + ddgf(e) * gfs + (int64_t)gy * L.px + gx + (int64_t)k * L.plane;
+        const double v = 8.0 * (__ldg(src + L.plane) - __ldg(src - L.plane)) -
+                         (__ldg(src + 2 * L.plane) - __ldg(src - 2 * L.plane));
+        if (f < 4 * FY) gzx[e * (FY * HXW) + jj * HXW + ii + 2] = v;
+        else gzy[e * (HYH * FX) + (jj + 2) * FX + ii] = v;
+      }
+      // ---- TMEM window shift (planes k-3 .. k+3) with the new plane k+3, and D1raw_z of the
+      // mixed GFs at the own point into the interior of the z helpers
+#pragma unroll
+      for (int q = 0; q < FEED0; ++q) {
+        const int gf = g_lo + q;
+        if (gf >= g_hi) continue;
+        uint32_t r[16];
+        tm_ld16(tb + 16u * (uint32_t)gf, r);
+        tm_wait_ld();
+        // old slots: planes k-4 .. k+2
+        const int e = ddi(gf);
+        if (e >= 0) {
+          const double v = 8.0 * (dbl(r[10], r[11]) - dbl(r[6], r[7])) - (dbl(r[12], r[13]) - dbl(r[4], r[5]));
+          gzx[e * (FY * HXW) + ty * HXW + tx + 2] = v;
+          gzy[e * (HYH * FX) + (ty + 2) * FX + tx] = v;
+        }
+        uint32_t w[16];
+#pragma unroll
+        for (int s = 0; s < 12; ++s) w[s] = r[s + 2];
+        w[12] = (uint32_t)__double2loint(feed[q]);
+        w[13] = (uint32_t)__double2hiint(feed[q]);
+        w[14] = w[15] = 0u;
+        tm_st16(tb + 16u * (uint32_t)gf, w);
+      }
+      tm_wait_st();
+      cta_sync_tm();
+      // ---- the RHS algebra of this thread's group from the on-chip derivatives, and its RK4
+      // update (pointwise operands from global memory, outputs + ghost images to global)
+      FusedP P{t, (ty + FR) * FSX + tx + FR, gzx, gzy, gyx, ty * HXW + tx + 2, (ty + 2) * FX + tx, tb};
+      const int64_t c = L.idx(i, j, k);
+      double r[NV];
+      if (grp == 0) {
+        bssn_point<2>(P, K, r);
+        if (live) bssn_update<STAGE, 2>(a, K, r, in, c, i, j, k, rhs_dst);
+      } else {
+        bssn_point<13>(P, K, r);
+        if (live) bssn_update<STAGE, 13>(a, K, r, in, c, i, j, k, rhs_dst);
+      }
+      cta_sync_tm();
+    }
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
+}
+
+template <int STAGE>
+cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cudaStream_t st) {
+  const Layout& L = a.L;
+  const int nk = a.k_end - a.k_begin;
+  if (nk <= 0) return cudaSuccess;
+  if (L.g < FR) return cudaErrorInvalidValue;
+  FusedMaps M;
+  const double* in = stage_input<STAGE>(a);
+  if (!encode_set_map(&M.in, in - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, FSX, FSY, NV))
+    return cudaErrorInvalidValue;
+  static std::atomic<uint64_t> attr_done{0};
+  if (cudaError_t e = smem_optin((const void*)bssn_fused<STAGE>, SMEM_FUSED, attr_done); e != cudaSuccess) return e;
+  const int nsm = device_sm_count();
+  const int ntx = (int)((L.nx + FX - 1) / FX), nty = (int)((L.ny + FY - 1) / FY);
+  const int ntiles = ntx * nty;
+  // z chunks: the fewest that fill the SMs in near-whole waves (each item re-reads a 7-plane
+  // window prologue, so longer chunks waste less)
+  int best_c = 1;
+  double best = -1.0;
+  for (int cnum = 1; cnum <= 8 && cnum <= nk; ++cnum) {
+    const int chunk = (nk + cnum - 1) / cnum;
+    const int items = ntiles * ((nk + chunk - 1) / chunk);
+    const int waves = (items + nsm - 1) / nsm;
+    const double eff = (double)items / ((double)waves * nsm) * (double)chunk / (chunk + 7.0);
+    if (eff > best + 1e-3) { best = eff; best_c = cnum; }
+  }
+  const int chunk = (nk + best_c - 1) / best_c;
+  const int nitems = ntiles * ((nk + chunk - 1) / chunk);
+  const int grid = nitems < nsm ? nitems : nsm;
+  bssn_fused<STAGE><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t bssn_fused_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
+  const BssnK K = make_k(a, a.hparams);
+  switch (stage) {
+    case 0: return launch_fused<0>(a, K, dst, st);
+    case 1: return launch_fused<1>(a, K, dst, st);
+    case 2: return launch_fused<2>(a, K, dst, st);
+    case 3: return launch_fused<3>(a, K, dst, st);
+    case 4: return launch_fused<4>(a, K, dst, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace chemora

@@ -567,7 +567,7 @@ int chemora_get_kernel_variant(chemora_grid_t g, int* variant) {
 int chemora_set_kernel_variant(chemora_grid_t g, int variant) {
   if (int rc = check_grid(g)) return rc;
   const bool ok = g->desc.system == CHEMORA_SYS_WAVE ? (variant >= 0 && variant <= 5) || variant == kVariantFused3
-                                                    : (variant == 0 || variant == 2 || variant == 3);
+                                                    : (variant == 0 || variant == 2 || variant == 3 || variant == 4);
   if (!ok) return fail(CHEMORA_E_INVALID, "unknown kernel variant " + std::to_string(variant));
   if (g->ipc) return fail(CHEMORA_E_PEER, "the kernel design of a peer-connected slab is fixed at connect time");
   g->variant = variant;

@@ -54,6 +54,9 @@ cudaError_t wave_tma_stage(const StageLaunch& a, int stage, cudaStream_t st);
 // BSSN (App. A) ------------------------------------------------------------------------
 cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st);
 cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
+// variant 4 (bssn_fused.cu): one fused kernel per stage, derivatives on chip (SMEM plane tiles
+// + TMEM z-windows); stage 0 = RHS only into dst
+cudaError_t bssn_fused_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st);
 // BSSN constraints H, M^i, G^i of a.s.y (R16): optional interior fields
 // [7][z][y][x] (nullable) and, on the device, out_dev[2q] = sum c_q^2, out_dev[2q+1] =
 // max |c_q| (scratch: kNormBlocks x 14 doubles).

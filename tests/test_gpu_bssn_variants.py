@@ -29,7 +29,7 @@ def relerr(a, b):
     return max(np.abs(a[f] - b[f]).max() / max(np.abs(b[f]).max(), 1e-6 * top) for f in range(b.shape[0]))
 
 
-@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("variant", [0, 2, 3, 4])
 @pytest.mark.parametrize("params", [BENCH, HARMONIC, GENERIC])
 def test_variant_parity(variant, params):
     P, C = _mods()
