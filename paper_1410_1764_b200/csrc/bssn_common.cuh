@@ -629,7 +629,7 @@ __device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K
 }
 
 template <int STAGE>
-__device__ __forceinline__ const double* stage_input(const StageLaunch& a) {
+__host__ __device__ __forceinline__ const double* stage_input(const StageLaunch& a) {
   return (STAGE <= 1) ? a.s.y : (STAGE == 2 ? a.s.b : (STAGE == 3 ? a.s.c : a.s.b));
 }
 

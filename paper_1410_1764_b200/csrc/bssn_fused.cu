@@ -7,8 +7,8 @@
 // the fused kernel too large is split across the SM's three on-chip stores instead:
 //
 //   * shared memory holds the current z-plane of ALL 25 GFs on a 16x8 tile with a 3-point
-//     halo (TMA 4-D box (22, 14, 1, 25), double-buffered so the next plane streams in while
-//     this one is used): every x and y stencil (D1, D2, upwind, mixed xy) reads it;
+//     halo (one TMA box (24, 14, 1, 1) per GF, double-buffered so the next plane streams in
+//     while this one is used): every x and y stencil (D1, D2, upwind, mixed xy) reads it;
 //   * TENSOR MEMORY holds each point's own z-column window, planes k-3 .. k+3 of all 25 GFs
 //     (TMEM lane = point, 16 columns per GF; 400 of the 512 columns), shifted by one plane per
 //     step: the z stencils (D1, D2, upwind) read it with one tcgen05.ld per GF;
@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 #include "bssn_common.cuh"
 #include "tma.cuh"
 
@@ -32,19 +33,33 @@ namespace {
 
 constexpr int FX = 16, FY = 8, FPT = FX * FY;          // tile points = TMEM lanes used
 constexpr int FR = 3;                                  // halo (upwind radius)
-constexpr int FSX = FX + 2 * FR, FSY = FY + 2 * FR, FPL = FSX * FSY;   // 22 x 14
+// the x halo is stored 4 wide so every TMA box row starts 16-byte aligned in global memory
+// (an odd fp64 start column faults the bulk-tensor copy) and spans 24 doubles
+constexpr int FRX = 4;
+constexpr int FSX = FX + 2 * FRX, FSY = FY + 2 * FR, FPL = FSX * FSY;   // 24 x 14
 constexpr int FNT = 2 * FPT;                           // (point, group) threads
 constexpr int NMIX = 11;                               // GFs with mixed second derivatives
 constexpr int HXW = FX + 4;                            // x-extended helper rows: i = -2 .. FX+1
 constexpr int HYH = FY + 4;                            // y-extended helper columns: j = -2 .. FY+1
-constexpr int TILE_BYTES = NV * FPL * 8;               // one plane of all GFs (61600 B)
-constexpr int TILE_STRIDE = (TILE_BYTES + 1023) / 1024 * 1024;
+constexpr int TILE_BYTES = NV * FPL * 8;               // one plane of all GFs (67200 B)
+constexpr int FPLS = (FPL * 8 + 127) / 128 * 16;       // GF plane stride in the tile: 128-byte aligned (336)
+constexpr int TILE_STRIDE = (NV * FPLS * 8 + 1023) / 1024 * 1024;
 constexpr int GZX_N = NMIX * FY * HXW, GZY_N = NMIX * HYH * FX, GYX_N = NMIX * FY * HXW;
 constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64;
 constexpr int FEED0 = 13;                              // group 0 feeds GFs [0, 13), group 1 [13, 25)
 constexpr int NFRAME = 2 * 2 * FY + 2 * 2 * FX;        // 2-point x- and y-frames of the tile: 96
 
 // ---- TMEM (tcgen05) helpers: each thread reads / writes its own lane
+#ifdef FUSED_NO_TMEM
+__device__ __forceinline__ void tm_ld16(uint32_t, uint32_t (&r)[16]) {
+  for (int q = 0; q < 16; ++q) r[q] = 0u;
+}
+__device__ __forceinline__ void tm_st16(uint32_t, const uint32_t (&)[16]) {}
+__device__ __forceinline__ void tm_wait_ld() {}
+__device__ __forceinline__ void tm_wait_st() {}
+__device__ __forceinline__ void tm_fence_before() {}
+__device__ __forceinline__ void tm_fence_after() {}
+#else
 __device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -64,6 +79,7 @@ __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sy
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+#endif
 __device__ __forceinline__ double dbl(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
 __device__ __forceinline__ void cta_sync_tm() {
   tm_fence_before();
@@ -88,20 +104,20 @@ __device__ __forceinline__ ZWin zwin(uint32_t tb, int gf) {
 // Derivative provider of the fused kernel (same operation order as StencilP: D1raw, D2raw,
 // D11raw with the outer sum along the first axis of the pair, ADVraw).
 struct FusedP {
-  const double* t;     // plane-k tile of all GFs, [gf][FSY][FSX]
+  const double* t;     // plane-k tile of all GFs, [gf][FSY][FSX], GF stride FPLS
   int c;               // own point's offset in a GF plane of the tile
   const double* gzx;   // [NMIX][FY][HXW]   D1raw_z, x-extended
   const double* gzy;   // [NMIX][HYH][FX]   D1raw_z, y-extended
   const double* gyx;   // [NMIX][FY][HXW]   D1raw_y, x-extended
   int hx, hy;          // own point's offsets in the x- / y-extended helper planes
   uint32_t tb;         // TMEM address of the point's lane, column 0
-  __device__ __forceinline__ double v(int gf) const { return t[gf * FPL + c]; }
+  __device__ __forceinline__ double v(int gf) const { return t[gf * FPLS + c]; }
   __device__ __forceinline__ double d1(const BssnK& K, int gf, int l) const {
     if (l == 2) {
       const ZWin z = zwin(tb, gf);
       return (8.0 * (z.w[4] - z.w[2]) - (z.w[5] - z.w[1])) * K.i12h[2];
     }
-    const double* f = t + gf * FPL + c;
+    const double* f = t + gf * FPLS + c;
     const int s = l == 0 ? 1 : FSX;
     return (8.0 * (f[s] - f[-s]) - (f[2 * s] - f[-2 * s])) * K.i12h[l];
   }
@@ -111,7 +127,7 @@ struct FusedP {
         const ZWin z = zwin(tb, gf);
         return (16.0 * (z.w[4] + z.w[2]) - (z.w[5] + z.w[1]) - 30.0 * f0) * K.i12h2[2];
       }
-      const double* f = t + gf * FPL + c;
+      const double* f = t + gf * FPLS + c;
       const int s = l == 0 ? 1 : FSX;
       return (16.0 * (f[s] + f[-s]) - (f[2 * s] + f[-2 * s]) - 30.0 * f0) * K.i12h2[l];
     }
@@ -124,7 +140,7 @@ struct FusedP {
     return (8.0 * (g[s] - g[-s]) - (g[2 * s] - g[-2 * s])) * K.i144hh[l + m - 1];
   }
   __device__ __forceinline__ double adv(const BssnK& K, int gf, const double* beta, double f0) const {
-    const double* f = t + gf * FPL + c;
+    const double* f = t + gf * FPLS + c;
     double r = 0.0;
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
@@ -164,10 +180,14 @@ __global__ void __launch_bounds__(FNT, 1)
   const double* in = stage_input<STAGE>(a);
   const int ntiles = ntx * nty;
 
+#ifndef FUSED_NO_TMEM
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+#else
+  if (tid == 0) *tmem_slot = 0;
+#endif
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -186,9 +206,16 @@ __global__ void __launch_bounds__(FNT, 1)
     ke = min(kb + chunk, a.k_end);
   };
   auto issue_tile = [&](int buf, int i0, int j0, int k) {
+#ifdef FUSED_NO_TMA
+    mbar_arrive(&mbar[buf]);
+    (void)i0; (void)j0; (void)k;
+#else
     mbar_arrive_expect_tx(&mbar[buf], (uint32_t)TILE_BYTES);
-    tma_load_4d(tiles + (size_t)buf * (TILE_STRIDE / 8), &M.in, &mbar[buf], kXOff + i0 - FR, L.g + j0 - FR,
-                L.g + k, 0);
+#pragma unroll 1
+    for (int q = 0; q < NV; ++q)  // one box per GF (a GF plane per 128-byte aligned slot)
+      tma_load_4d(tiles + (size_t)buf * (TILE_STRIDE / 8) + q * FPLS, &M.in, &mbar[buf], kXOff + i0 - FRX,
+                  L.g + j0 - FR, L.g + k, q);
+#endif
   };
   const int64_t gfs = L.gfs;
   const int xlo = -L.g, xhi = (int)L.nx + L.g - 1, ylo = -L.g, yhi = (int)L.ny + L.g - 1;
@@ -204,10 +231,13 @@ __global__ void __launch_bounds__(FNT, 1)
     item_geom(it, i0, j0, kb, ke);
     const int i = i0 + tx, j = j0 + ty;
     const bool live = i < L.nx && j < L.ny;
-    const int ic = min(i, (int)L.nx - 1), jc = min(j, (int)L.ny - 1);  // dead lanes: a valid column
+    // dead lanes (past the interior of a ragged tile) keep their own column while it lies in
+    // the ghost zone: live neighbours read their D1_z through the mixed-derivative helpers
+    const int ic = min(i, xhi), jc = min(j, yhi);
     const double* col = in + (int64_t)jc * L.px + ic;                   // own column, plane 0, GF 0
     const int g_lo = grp == 0 ? 0 : FEED0, g_hi = grp == 0 ? FEED0 : NV;
     // ---- window fill: planes kb-4 .. kb+2 into slots 0..6 (slot 0 is dropped by the first shift)
+    __syncwarp();
     for (int gf = g_lo; gf < g_hi; ++gf) {
       uint32_t r[16];
 #pragma unroll
@@ -247,7 +277,7 @@ __global__ void __launch_bounds__(FNT, 1)
       for (int q = tid; q < GYX_N; q += FNT) {
         const int e = q / (FY * HXW), rem = q % (FY * HXW);
         const int jj = rem / HXW, ii = rem % HXW - 2;
-        const double* f = t + ddgf(e) * FPL + (jj + FR) * FSX + (ii + FR);
+        const double* f = t + ddgf(e) * FPLS + (jj + FR) * FSX + (ii + FRX);
         gyx[q] = 8.0 * (f[FSX] - f[-FSX]) - (f[2 * FSX] - f[-2 * FSX]);
       }
       // ---- helper: D1raw_z on the 2-point frame around the tile (from L2)
@@ -264,7 +294,9 @@ __global__ void __launch_bounds__(FNT, 1)
         else gzy[e * (HYH * FX) + (jj + 2) * FX + ii] = v;
       }
       // ---- TMEM window shift (planes k-3 .. k+3) with the new plane k+3, and D1raw_z of the
-      // mixed GFs at the own point into the interior of the z helpers
+      // mixed GFs at the own point into the interior of the z helpers.  tcgen05.ld/st are
+      // .sync.aligned: reconverge the warp after the thread-dependent helper loops first
+      __syncwarp();
 #pragma unroll
       for (int q = 0; q < FEED0; ++q) {
         const int gf = g_lo + q;
@@ -291,7 +323,7 @@ __global__ void __launch_bounds__(FNT, 1)
       cta_sync_tm();
       // ---- the RHS algebra of this thread's group from the on-chip derivatives, and its RK4
       // update (pointwise operands from global memory, outputs + ghost images to global)
-      FusedP P{t, (ty + FR) * FSX + tx + FR, gzx, gzy, gyx, ty * HXW + tx + 2, (ty + 2) * FX + tx, tb};
+      FusedP P{t, (ty + FR) * FSX + tx + FRX, gzx, gzy, gyx, ty * HXW + tx + 2, (ty + 2) * FX + tx, tb};
       const int64_t c = L.idx(i, j, k);
       double r[NV];
       if (grp == 0) {
@@ -304,7 +336,9 @@ __global__ void __launch_bounds__(FNT, 1)
       cta_sync_tm();
     }
   }
+#ifndef FUSED_NO_TMEM
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
+#endif
 }
 
 template <int STAGE>
@@ -313,12 +347,21 @@ cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cuda
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
   if (L.g < FR) return cudaErrorInvalidValue;
+#ifdef CHEMORA_DEBUG_FUSED
+  fprintf(stderr, "launch_fused<%d> enter\n", STAGE);
+#endif
   FusedMaps M;
   const double* in = stage_input<STAGE>(a);
-  if (!encode_set_map(&M.in, in - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, FSX, FSY, NV))
+  if (!encode_set_map(&M.in, in - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, FSX, FSY, 1))
     return cudaErrorInvalidValue;
+#ifdef CHEMORA_DEBUG_FUSED
+  fprintf(stderr, "launch_fused<%d> encoded\n", STAGE);
+#endif
   static std::atomic<uint64_t> attr_done{0};
   if (cudaError_t e = smem_optin((const void*)bssn_fused<STAGE>, SMEM_FUSED, attr_done); e != cudaSuccess) return e;
+#ifdef CHEMORA_DEBUG_FUSED
+  fprintf(stderr, "launch_fused<%d> optin\n", STAGE);
+#endif
   const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + FX - 1) / FX), nty = (int)((L.ny + FY - 1) / FY);
   const int ntiles = ntx * nty;
@@ -336,7 +379,18 @@ cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cuda
   const int chunk = (nk + best_c - 1) / best_c;
   const int nitems = ntiles * ((nk + chunk - 1) / chunk);
   const int grid = nitems < nsm ? nitems : nsm;
+#ifdef CHEMORA_DEBUG_FUSED
+  fprintf(stderr, "launch_fused<%d> grid %d items %d chunk %d smem %d\n", STAGE, grid, nitems, chunk, SMEM_FUSED);
+#endif
   bssn_fused<STAGE><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+#ifdef CHEMORA_DEBUG_FUSED
+  {
+    cudaError_t e1 = cudaGetLastError();
+    cudaError_t e2 = cudaDeviceSynchronize();
+    fprintf(stderr, "launch_fused<%d>: launch %s, sync %s\n", STAGE, cudaGetErrorString(e1), cudaGetErrorString(e2));
+    return e1 != cudaSuccess ? e1 : e2;
+  }
+#endif
   return cudaGetLastError();
 }
 
