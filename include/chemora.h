@@ -228,20 +228,27 @@ int chemora_set_phase_barrier(chemora_grid_t grid, void (*fn)(void* user), void*
 
 /* ---- analysis and tuning */
 
-/* Fused energy monitor (wave only; Fig. 1 "Energy" eps = 1/2 (rho^2 + delta^ij v_i v_j),
+/* Fused monitors.  WAVE: energy (Fig. 1 "Energy" eps = 1/2 (rho^2 + delta^ij v_i v_j),
  * PAPER.md:642-644): when enabled, the kernel of every chemora_rk4_step(_multi) step that
  * writes the new state (the stage-4 kernel, or the stage-pair kernel B of the temporally
  * blocked path) also reduces E = h^3 sum eps of that state over the LOCAL slab
  * (deterministic per-CTA partials + a fixed-order sum) -- no extra HBM pass over the state.
- * With nranks > 1 the global energy is the sum of the slabs' values (the Python Grid /
- * LocalSlabs helpers add them in rank order). */
+ * BSSN: the constraint monitors H, M^i, G^i (R16) of the state
+ * entering every step, reduced by the step's stage-1 kernel (kernel design 4: from the
+ * derivatives it computes anyway; other designs: the constraint kernel before stage 1).
+ * Read with chemora_read_monitor (global values, collective for nranks > 1) or
+ * chemora_read_monitor_multi (same-process slabs). */
 int chemora_set_monitor(chemora_grid_t grid, int enable);
 
-/* Copy up to max per-step energies recorded since the last read (oldest first) to out;
- * *count receives the number copied.  Synchronises the stream.  The device ring holds 1024
- * steps; reading less often is an error (CHEMORA_E_INVALID).  nranks > 1 (IPC ring):
- * COLLECTIVE, the values are the global energies (the slabs' values all-gathered and added
- * in rank order), identical on every rank. */
+/* Copy the monitor values of up to max steps recorded since the last read (oldest first) to
+ * out; *count receives the number of steps.  WAVE: one double per step, the energy after the
+ * step.  BSSN: 14 doubles per step, [L2 = sqrt(h^3 sum c^2), Linf] of H, M1..3, G1..3 (the
+ * constraints of chemora_constraints) of the state ENTERING the step -- computed by the
+ * fused stage-1 kernel of kernel design 4 from the derivatives it already holds on chip (no
+ * extra pass over the state; other designs run the constraint kernel before stage 1).
+ * Synchronises the stream.  The device ring holds 1024 steps; reading less often is an error
+ * (CHEMORA_E_INVALID).  nranks > 1 (IPC ring): COLLECTIVE, the values are global (the slabs'
+ * partials all-gathered and combined in rank order), identical on every rank. */
 int chemora_read_monitor(chemora_grid_t grid, double* out, int32_t max, int32_t* count,
                          void* stream);
 /* The same for n same-process slabs (chemora_grid_connect_local): slab values added in slab

@@ -281,21 +281,25 @@ def chemora_set_monitor(h, enable: bool):
     _check(_lib.chemora_set_monitor(h, 1 if enable else 0), "chemora_set_monitor")
 
 
-def chemora_read_monitor(h, max_steps: int = 1024, stream=None) -> np.ndarray:
-    out = np.zeros(max(1, max_steps))
+def chemora_read_monitor(h, max_steps: int = 1024, stream=None, width: int = 1) -> np.ndarray:
+    """Per-step monitor values since the last read: width 1 (wave energies) -> shape (n,);
+    width 14 (BSSN [L2, Linf] x (H, M1..3, G1..3)) -> shape (n, 14)."""
+    out = np.zeros(max(1, max_steps) * width)
     cnt = ctypes.c_int32()
     _check(_lib.chemora_read_monitor(h, _dptr(out), max_steps, ctypes.byref(cnt), stream),
            "chemora_read_monitor")
-    return out[:cnt.value].copy()
+    out = out[:cnt.value * width].copy()
+    return out if width == 1 else out.reshape(cnt.value, width)
 
 
-def chemora_read_monitor_multi(handles, max_steps: int = 1024, stream=None) -> np.ndarray:
+def chemora_read_monitor_multi(handles, max_steps: int = 1024, stream=None, width: int = 1) -> np.ndarray:
     arr = (_vp * len(handles))(*handles)
-    out = np.zeros(max(1, max_steps))
+    out = np.zeros(max(1, max_steps) * width)
     cnt = ctypes.c_int32()
     _check(_lib.chemora_read_monitor_multi(arr, len(handles), _dptr(out), max_steps, ctypes.byref(cnt), stream),
            "chemora_read_monitor_multi")
-    return out[:cnt.value].copy()
+    out = out[:cnt.value * width].copy()
+    return out if width == 1 else out.reshape(cnt.value, width)
 
 
 def chemora_set_launch_timing(h, enable: bool):

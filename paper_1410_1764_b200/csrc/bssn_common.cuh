@@ -414,7 +414,9 @@ __device__ __forceinline__ void bssn_point(const P& D, const BssnK& K, double* r
 //            (the full conformal divergence D~_j At^ij: det gt is not assumed 1)
 //   c[4+i] = G^i = Xt^i - gt^jk Gt^i_jk
 // d_j At^ij by the product rule with d_j gt^ab = -gt^ac (d_j gt_cd) gt^db.
-__device__ __forceinline__ void bssn_constraint_point(const StencilP& D, const BssnK& K, double* c) {
+// PART: 0 = all seven, 1 = the Hamiltonian only (c[0]), 2 = momentum and Gamma only (c[1..6]).
+template <int PART = 0, class P = StencilP>
+__device__ __forceinline__ void bssn_constraint_point(const P& D, const BssnK& K, double* c) {
   double gt[6], At[6];
 #pragma unroll
   for (int s = 0; s < 6; ++s) { gt[s] = D.v(V_GT + s); At[s] = D.v(V_AT + s); }
@@ -469,7 +471,7 @@ __device__ __forceinline__ void bssn_constraint_point(const StencilP& D, const B
     Au[s] = Am[i][0] * gu[sy(0, j)] + Am[i][1] * gu[sy(1, j)] + Am[i][2] * gu[sy(2, j)];
   }
   // ---- Hamiltonian: Ricci scalar as in bssn_point's curvature group
-  {
+  if (PART != 2) {
     double Rt[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) Rt[s] = 0.0;
@@ -522,6 +524,7 @@ __device__ __forceinline__ void bssn_constraint_point(const StencilP& D, const B
     c[0] = exp(-4.0 * phi) * Rsum + (2.0 / 3.0) * trK * trK - AA;
   }
   // ---- momentum and Gamma constraints
+  if (PART == 1) return;
   double W[3] = {0.0, 0.0, 0.0}, U[3] = {0.0, 0.0, 0.0}, V[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
@@ -577,11 +580,34 @@ BssnK make_k(const StageLaunch& a, const double* prm) {
   return K;
 }
 
-// RK4 stage update of the GFs of group G at point c (interior (i,j,k)) and the stores.
+// Source of the stage input's value of GF v at the point: global memory (default) or a
+// copy the kernel already holds on chip (bssn_fused.cu: the shared-memory plane tile).
+struct GmemIn {
+  const double* in;
+  int64_t c, gfs;
+  __device__ __forceinline__ double operator()(int v) const { return __ldg(in + v * gfs + c); }
+};
+template <int STAGE, int G, class IN, bool XYONLY = false>
+__device__ __forceinline__ void bssn_update_src(const StageLaunch& a, const BssnK& K, const double* r,
+                                                const IN& insrc, int64_t c, int i, int j, int k,
+                                                double* rhs_dst);
 template <int STAGE, int G>
 __device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K, const double* r,
                                             const double* in, int64_t c, int i, int j, int k,
                                             double* rhs_dst) {
+  GmemIn src;
+  src.in = in;
+  src.c = c;
+  src.gfs = a.L.gfs;
+  bssn_update_src<STAGE, G>(a, K, r, src, c, i, j, k, rhs_dst);
+}
+// RK4 stage update of the GFs of group G at point c (interior (i,j,k)) and the stores.
+// XYONLY: store only the x/y periodic images inline (the launcher pushes the z ghost planes,
+// x/y images included, with a separate plane copy after the kernel).
+template <int STAGE, int G, class IN, bool XYONLY>
+__device__ __forceinline__ void bssn_update_src(const StageLaunch& a, const BssnK& K, const double* r,
+                                                const IN& insrc, int64_t c, int i, int j, int k,
+                                                double* rhs_dst) {
   const Layout& L = a.L;
   const int64_t gfs = L.gfs;
   if (STAGE == 0) {
@@ -594,7 +620,12 @@ __device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K
   }
   double* out = STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y));
   const FaceDst fd = a.img[STAGE - 1];
-  const bool nf = near_face(L, i, j, k);
+  // ghost images: a point near exactly one x or y face stores its one periodic image inline;
+  // z faces and x-y edges (3 % of the points at 192^3) take the out-of-line general routine
+  const ImageSite isite = image_site(L, i, j, k);
+  const int gw = L.g;
+  const int64_t ddx = i < gw ? L.nx : (i >= L.nx - gw ? -L.nx : 0);
+  const int64_t ddy = (j < gw ? L.ny : (j >= L.ny - gw ? -L.ny : 0)) * L.px;
   const unsigned long long code0 = a.step * (unsigned long long)NV;
   // all pointwise operands of the group first: the output stores below may alias them (plain
   // pointers), so loads interleaved with the stores would serialise one memory round trip
@@ -604,10 +635,10 @@ __device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K
   for (int v = 0; v < NV; ++v) {
     if (!in_group(G, v)) continue;
     const int64_t o = v * gfs + c;
-    if (STAGE == 1) p0[v] = ld(in + o);
-    if (STAGE == 2) { p0[v] = ld(a.s.y + o); p1[v] = ld(in + o); }
+    if (STAGE == 1) p0[v] = insrc(v);
+    if (STAGE == 2) { p0[v] = ld(a.s.y + o); p1[v] = insrc(v); }
     if (STAGE == 3) p0[v] = ld(a.s.y + o);
-    if (STAGE == 4) { p0[v] = ld(in + o); p1[v] = ld(a.s.q + o); }
+    if (STAGE == 4) { p0[v] = insrc(v); p1[v] = ld(a.s.q + o); }
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -623,7 +654,13 @@ __device__ __forceinline__ void bssn_update(const StageLaunch& a, const BssnK& K
     if (STAGE == 3) val = fma(K.dt, r[v], p0[v]);
     if (STAGE == 4) val = fma(K.dt6, r[v], fma(p0[v], K.third, p1[v]));
     out[o] = val;
-    if (nf) store_images(out + v * gfs, fd.lo + v * gfs, fd.hi + v * gfs, L, i, j, k, val);
+    if (XYONLY) {
+      if (ddx) out[o + ddx] = val;
+      if (ddy) out[o + ddy] = val;
+      if (ddx && ddy) out[o + ddx + ddy] = val;
+    } else {
+      put_images(isite, out + v * gfs, fd.lo + v * gfs, fd.hi + v * gfs, L, i, j, k, c, val);
+    }
     if (STAGE == 4) check_finite(a.nan_flag, code0 + v, val);
   }
 }

@@ -37,7 +37,14 @@ constexpr int FR = 3;                                  // halo (upwind radius)
 // (an odd fp64 start column faults the bulk-tensor copy) and spans 24 doubles
 constexpr int FRX = 4;
 constexpr int FSX = FX + 2 * FRX, FSY = FY + 2 * FR, FPL = FSX * FSY;   // 24 x 14
-constexpr int FNT = 2 * FPT;                           // (point, group) threads
+#ifndef FUSED_NGRP
+#define FUSED_NGRP 2
+#endif
+// equation groups per point: 2 = {G2, G13} at 255 registers (8 warps/SM); 3 = {G2, G1, G3} at
+// 168 registers (12 warps/SM)
+constexpr int NGRP = FUSED_NGRP;
+constexpr int FNT = NGRP * FPT;                        // (point, group) threads
+constexpr int NWARP = FNT / 32;
 constexpr int NMIX = 11;                               // GFs with mixed second derivatives
 constexpr int HXW = FX + 4;                            // x-extended helper rows: i = -2 .. FX+1
 constexpr int HYH = FY + 4;                            // y-extended helper columns: j = -2 .. FY+1
@@ -45,9 +52,14 @@ constexpr int TILE_BYTES = NV * FPL * 8;               // one plane of all GFs (
 constexpr int FPLS = (FPL * 8 + 127) / 128 * 16;       // GF plane stride in the tile: 128-byte aligned (336)
 constexpr int TILE_STRIDE = (NV * FPLS * 8 + 1023) / 1024 * 1024;
 constexpr int GZX_N = NMIX * FY * HXW, GZY_N = NMIX * HYH * FX, GYX_N = NMIX * FY * HXW;
-constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64;
-constexpr int FEED0 = 13;                              // group 0 feeds GFs [0, 13), group 1 [13, 25)
+constexpr int NMON = 14;                               // constraint monitor: [sum c_q^2, max|c_q|] x 7
+constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64 + 8 * NWARP * NMON;
+// TMEM window feed split over the groups: [0, 9) [9, 17) [17, 25) (3 groups) or [0, 13) [13, 25)
+// -- the 11 GFs with mixed derivatives stay with one group each (phi, gt: 0; alpha, beta: last)
+constexpr int FEED_B1 = NGRP == 3 ? 9 : 13, FEED_B2 = NGRP == 3 ? 17 : 25;
+constexpr int FEEDN = NGRP == 3 ? 9 : 13;             // max GFs fed by one thread
 constexpr int NFRAME = 2 * 2 * FY + 2 * 2 * FX;        // 2-point x- and y-frames of the tile: 96
+constexpr int NFI = (NMIX * NFRAME + FNT - 1) / FNT;   // frame items per thread (5)
 
 // ---- TMEM (tcgen05) helpers: each thread reads / writes its own lane
 #ifdef FUSED_NO_TMEM
@@ -157,6 +169,13 @@ struct FusedP {
   }
 };
 
+// stage-input values at the point from the shared plane tile (RK update operands)
+struct TileIn {
+  const double* t;
+  int c;
+  __device__ __forceinline__ double operator()(int v) const { return t[v * FPLS + c]; }
+};
+
 struct FusedMaps {
   CUtensorMap in;  // the stage input set, box (FSX, FSY, 1, NV)
 };
@@ -172,11 +191,14 @@ __global__ void __launch_bounds__(FNT, 1)
   double* gyx = gzy + GZY_N;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(gyx + GYX_N);           // 2 mbarriers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+  double* macc = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64);  // [8][NMON]
+  const bool monitor = STAGE == 1 && a.mon_partials != nullptr;
   const Layout& L = a.L;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int grp = warp >> 2;                     // 0: G2, 1: G13
+  const int grp = warp >> 2;                     // 0: G2; 1: G13 (2 groups) or G1; 2: G3
   const int p = (warp & 3) * 32 + lane;          // point of the tile (= TMEM lane)
   const int tx = p % FX, ty = p / FX;
+  if (monitor && tid < NWARP * NMON) macc[tid] = 0.0;  // ordered before use by the first CTA barrier
   const double* in = stage_input<STAGE>(a);
   const int ntiles = ntx * nty;
 
@@ -235,7 +257,20 @@ __global__ void __launch_bounds__(FNT, 1)
     // the ghost zone: live neighbours read their D1_z through the mixed-derivative helpers
     const int ic = min(i, xhi), jc = min(j, yhi);
     const double* col = in + (int64_t)jc * L.px + ic;                   // own column, plane 0, GF 0
-    const int g_lo = grp == 0 ? 0 : FEED0, g_hi = grp == 0 ? FEED0 : NV;
+    const int g_lo = grp == 0 ? 0 : (grp == 1 ? FEED_B1 : FEED_B2);
+    const int g_hi = grp == 0 ? FEED_B1 : (grp == 1 ? FEED_B2 : NV);
+    // frame item geometry of this thread, recomputed per plane (cheap integer work; keeping
+    // it live across the algebra would cost registers)
+    auto frame_item = [&](int m, int& dst) -> int64_t {
+      const int q = tid + m * FNT;
+      const int e = q / NFRAME, f = q % NFRAME;
+      int ii, jj;
+      if (f < 4 * FY) { jj = f >> 2; const int cc = f & 3; ii = cc < 2 ? cc - 2 : FX + cc - 2; }
+      else { const int f2 = f - 4 * FY; ii = f2 % FX; const int rr = f2 / FX; jj = rr < 2 ? rr - 2 : FY + rr - 2; }
+      const int gx = min(max(i0 + ii, xlo), xhi), gy = min(max(j0 + jj, ylo), yhi);
+      dst = f < 4 * FY ? e * (FY * HXW) + jj * HXW + ii + 2 : GZX_N + e * (HYH * FX) + (jj + 2) * FX + ii;
+      return ddgf(e) * gfs + (int64_t)gy * L.px + gx;
+    };
     // ---- window fill: planes kb-4 .. kb+2 into slots 0..6 (slot 0 is dropped by the first shift)
     __syncwarp();
     for (int gf = g_lo; gf < g_hi; ++gf) {
@@ -263,10 +298,38 @@ __global__ void __launch_bounds__(FNT, 1)
           issue_tile(buf ^ 1, ni0, nj0, nkb);
         }
       }
-      // ---- own-column values of plane k+3 for this thread's GF half (consumed by the shift)
-      double feed[NV - FEED0 > FEED0 ? NV - FEED0 : FEED0];
+      // ---- all global loads of the plane first (one exposed latency): the D1_z frame operands
+      // (planes k+-1, k+-2 around the tile, L2-resident) ...
+      double fv[NFI][4];
+      int fdst[NFI];
 #pragma unroll
-      for (int q = 0; q < FEED0; ++q) {
+      for (int m = 0; m < NFI; ++m)
+        if (tid + m * FNT < NMIX * NFRAME) {
+          const double* s0 = in + frame_item(m, fdst[m]) + (int64_t)k * L.plane;
+          fv[m][0] = __ldg(s0 - 2 * L.plane);
+          fv[m][1] = __ldg(s0 - L.plane);
+          fv[m][2] = __ldg(s0 + L.plane);
+          fv[m][3] = __ldg(s0 + 2 * L.plane);
+        }
+      // ... the RK update's pointwise operands of y / Q pulled into L1 ...
+      if (STAGE >= 2 && STAGE <= 4 && live) {
+        const double* pre = (STAGE == 4 ? a.s.q : a.s.y) + L.idx(i, j, k);
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (grp == 0 ? in_group(2, v) : (NGRP == 2 ? in_group(13, v) : (grp == 1 ? in_group(1, v) : in_group(3, v))))
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pre + v * gfs));
+      }
+      // ... the own column two planes ahead of the feed pulled into L2 (its first touch is
+      // an HBM round trip) ...
+      {
+        const int kp = min(k + 5, (int)L.nz + L.g - 1);
+        for (int gf = g_lo; gf < g_hi; ++gf)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(col + gf * gfs + (int64_t)kp * L.plane));
+      }
+      // ... and the own-column values of plane k+3 for this thread's GF half (for the shift)
+      double feed[FEEDN];
+#pragma unroll
+      for (int q = 0; q < FEEDN; ++q) {
         const int gf = g_lo + q;
         if (gf < g_hi) feed[q] = __ldg(col + gf * gfs + (int64_t)(k + 3) * L.plane);
       }
@@ -280,25 +343,16 @@ __global__ void __launch_bounds__(FNT, 1)
         const double* f = t + ddgf(e) * FPLS + (jj + FR) * FSX + (ii + FRX);
         gyx[q] = 8.0 * (f[FSX] - f[-FSX]) - (f[2 * FSX] - f[-2 * FSX]);
       }
-      // ---- helper: D1raw_z on the 2-point frame around the tile (from L2)
-      for (int q = tid; q < NMIX * NFRAME; q += FNT) {
-        const int e = q / NFRAME, f = q % NFRAME;
-        int ii, jj;
-        if (f < 4 * FY) { jj = f >> 2; const int cc = f & 3; ii = cc < 2 ? cc - 2 : FX + cc - 2; }
-        else { const int f2 = f - 4 * FY; ii = f2 % FX; const int rr = f2 / FX; jj = rr < 2 ? rr - 2 : FY + rr - 2; }
-        const int gx = min(max(i0 + ii, xlo), xhi), gy = min(max(j0 + jj, ylo), yhi);
-        const double* src = in + ddgf(e) * gfs + (int64_t)gy * L.px + gx + (int64_t)k * L.plane;
-        const double v = 8.0 * (__ldg(src + L.plane) - __ldg(src - L.plane)) -
-                         (__ldg(src + 2 * L.plane) - __ldg(src - 2 * L.plane));
-        if (f < 4 * FY) gzx[e * (FY * HXW) + jj * HXW + ii + 2] = v;
-        else gzy[e * (HYH * FX) + (jj + 2) * FX + ii] = v;
-      }
+      // ---- helper: D1raw_z on the 2-point frame around the tile (operands loaded above)
+#pragma unroll
+      for (int m = 0; m < NFI; ++m)
+        if (tid + m * FNT < NMIX * NFRAME) gzx[fdst[m]] = 8.0 * (fv[m][2] - fv[m][1]) - (fv[m][3] - fv[m][0]);
       // ---- TMEM window shift (planes k-3 .. k+3) with the new plane k+3, and D1raw_z of the
       // mixed GFs at the own point into the interior of the z helpers.  tcgen05.ld/st are
       // .sync.aligned: reconverge the warp after the thread-dependent helper loops first
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < FEED0; ++q) {
+      for (int q = 0; q < FEEDN; ++q) {
         const int gf = g_lo + q;
         if (gf >= g_hi) continue;
         uint32_t r[16];
@@ -326,12 +380,43 @@ __global__ void __launch_bounds__(FNT, 1)
       FusedP P{t, (ty + FR) * FSX + tx + FRX, gzx, gzy, gyx, ty * HXW + tx + 2, (ty + 2) * FX + tx, tb};
       const int64_t c = L.idx(i, j, k);
       double r[NV];
+      const TileIn tin{t, P.c};
       if (grp == 0) {
         bssn_point<2>(P, K, r);
-        if (live) bssn_update<STAGE, 2>(a, K, r, in, c, i, j, k, rhs_dst);
-      } else {
+        if (live) bssn_update_src<STAGE, 2, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
+      } else if (NGRP == 2) {
         bssn_point<13>(P, K, r);
-        if (live) bssn_update<STAGE, 13>(a, K, r, in, c, i, j, k, rhs_dst);
+        if (live) bssn_update_src<STAGE, 13, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
+      } else if (grp == 1) {
+        bssn_point<1>(P, K, r);
+        if (live) bssn_update_src<STAGE, 1, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
+      } else {
+        bssn_point<3>(P, K, r);
+        if (live) bssn_update_src<STAGE, 3, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
+      }
+      if constexpr (STAGE == 1) {
+        // NEXT-3 fused constraint monitor: H, M^i, G^i of the state entering
+        // this step (stage 1's input, already on chip), reduced per warp in a fixed order
+        if (monitor && (grp == 0 || grp == NGRP - 1)) {  // H by the G2 warps, M and G by the last group
+          double cv[7];
+          if (grp == 0) bssn_constraint_point<1>(P, K, cv);
+          else bssn_constraint_point<2>(P, K, cv);
+#pragma unroll
+          for (int q = 0; q < 7; ++q) {
+            if ((grp == 0) != (q == 0)) continue;
+            const double v = live ? cv[q] : 0.0;
+            double s2 = v * v, mx = fabs(v);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+              mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if (lane == 0) {
+              macc[warp * NMON + 2 * q] += s2;
+              macc[warp * NMON + 2 * q + 1] = fmax(macc[warp * NMON + 2 * q + 1], mx);
+            }
+          }
+        }
       }
       cta_sync_tm();
     }
@@ -339,6 +424,37 @@ __global__ void __launch_bounds__(FNT, 1)
 #ifndef FUSED_NO_TMEM
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
 #endif
+  if (monitor && tid < NMON) {  // warps in order: deterministic per-CTA partials
+    double v = macc[tid];
+    for (int w = 1; w < NWARP; ++w) v = (tid & 1) ? fmax(v, macc[w * NMON + tid]) : v + macc[w * NMON + tid];
+    a.mon_partials[(int64_t)blockIdx.x * NMON + tid] = v;
+  }
+}
+
+// z chunks: the fewest that fill the SMs in near-whole waves (each item re-reads a 7-plane
+// window prologue, so longer chunks waste less); grid = min(items, SMs)
+struct FusedPlan {
+  int ntx, nty, chunk, nitems, grid;
+};
+FusedPlan fused_plan(const Layout& L, int nk) {
+  FusedPlan p;
+  const int nsm = device_sm_count();
+  p.ntx = (int)((L.nx + FX - 1) / FX);
+  p.nty = (int)((L.ny + FY - 1) / FY);
+  const int ntiles = p.ntx * p.nty;
+  int best_c = 1;
+  double best = -1.0;
+  for (int cnum = 1; cnum <= 8 && cnum <= nk; ++cnum) {
+    const int chunk = (nk + cnum - 1) / cnum;
+    const int items = ntiles * ((nk + chunk - 1) / chunk);
+    const int waves = (items + nsm - 1) / nsm;
+    const double eff = (double)items / ((double)waves * nsm) * (double)chunk / (chunk + 7.0);
+    if (eff > best + 1e-3) { best = eff; best_c = cnum; }
+  }
+  p.chunk = (nk + best_c - 1) / best_c;
+  p.nitems = ntiles * ((nk + p.chunk - 1) / p.chunk);
+  p.grid = p.nitems < nsm ? p.nitems : nsm;
+  return p;
 }
 
 template <int STAGE>
@@ -362,27 +478,16 @@ cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cuda
 #ifdef CHEMORA_DEBUG_FUSED
   fprintf(stderr, "launch_fused<%d> optin\n", STAGE);
 #endif
-  const int nsm = device_sm_count();
-  const int ntx = (int)((L.nx + FX - 1) / FX), nty = (int)((L.ny + FY - 1) / FY);
-  const int ntiles = ntx * nty;
-  // z chunks: the fewest that fill the SMs in near-whole waves (each item re-reads a 7-plane
-  // window prologue, so longer chunks waste less)
-  int best_c = 1;
-  double best = -1.0;
-  for (int cnum = 1; cnum <= 8 && cnum <= nk; ++cnum) {
-    const int chunk = (nk + cnum - 1) / cnum;
-    const int items = ntiles * ((nk + chunk - 1) / chunk);
-    const int waves = (items + nsm - 1) / nsm;
-    const double eff = (double)items / ((double)waves * nsm) * (double)chunk / (chunk + 7.0);
-    if (eff > best + 1e-3) { best = eff; best_c = cnum; }
-  }
-  const int chunk = (nk + best_c - 1) / best_c;
-  const int nitems = ntiles * ((nk + chunk - 1) / chunk);
-  const int grid = nitems < nsm ? nitems : nsm;
+  const FusedPlan p = fused_plan(L, nk);
+  const int ntx = p.ntx, nty = p.nty, chunk = p.chunk, nitems = p.nitems, grid = p.grid;
 #ifdef CHEMORA_DEBUG_FUSED
   fprintf(stderr, "launch_fused<%d> grid %d items %d chunk %d smem %d\n", STAGE, grid, nitems, chunk, SMEM_FUSED);
 #endif
   bssn_fused<STAGE><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+  if (STAGE >= 1) {  // z ghost planes of the stage output (own wrap or the neighbours' slabs)
+    double* out = const_cast<double*>(STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y)));
+    if (cudaError_t e = push_z_planes(L, out, a.img[STAGE - 1], st); e != cudaSuccess) return e;
+  }
 #ifdef CHEMORA_DEBUG_FUSED
   {
     cudaError_t e1 = cudaGetLastError();
@@ -395,6 +500,8 @@ cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cuda
 }
 
 }  // namespace
+
+int bssn_fused_grid(const Layout& L, int nk) { return fused_plan(L, nk).grid; }
 
 cudaError_t bssn_fused_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st) {
   const BssnK K = make_k(a, a.hparams);

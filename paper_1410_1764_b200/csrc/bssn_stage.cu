@@ -488,6 +488,11 @@ cudaError_t bssn_stage(const StageLaunch& a, int stage, cudaStream_t st) {
 cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st) {
   return dispatch(a, 0, dst, st, a.hparams);
 }
+cudaError_t bssn_constraints_reduce(const double* part, int nblocks, double* out14, cudaStream_t st) {
+  bssn_constraints_combine<<<1, 32, 0, st>>>(part, nblocks, out14);
+  return cudaGetLastError();
+}
+
 cudaError_t bssn_constraints(const StageLaunch& a, double* fields, double* scratch, double* out_dev,
                              cudaStream_t st) {
   const BssnK K = make_k(a, a.hparams);

@@ -147,7 +147,9 @@ size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 // workspace: [sets][norm scratch][norm out][params][flags][monitor][table][gather]
 constexpr int kMonHist = 1024;  // energy-monitor ring (steps)
-constexpr int kGatherLen = kMonHist;  // doubles per rank slot of the collective gather
+constexpr int kMonCtas = 1024;        // max CTAs of the BSSN stage-1 launch
+int mon_width(int system) { return system == CHEMORA_SYS_BSSN ? 14 : 1; }  // ring entry width
+constexpr int kGatherLen = kMonHist * 14;  // doubles per rank slot of the collective gather
 constexpr int kBssnTab = 136;   // BSSN derivative-table slots per point (bssn_stage.cu variant 3)
 struct WsPlan {
   size_t sets, scratch, out, params, flags, mon, hist, tab, gather, total;
@@ -172,11 +174,13 @@ WsPlan plan_ws(const Layout& L, int system, int nranks) {
   if (system == CHEMORA_SYS_WAVE) {
     const int64_t ntx = (L.nx + 31) / 32;
     p.mon_n = ntx * (L.ny * L.nz / 8 + L.ny + L.nz + 1);
+  } else {
+    p.mon_n = (int64_t)kMonCtas * 14;  // BSSN: per-CTA constraint partials of the stage-1 kernel
   }
   p.mon = off;
   off += align256(sizeof(double) * (size_t)p.mon_n);
   p.hist = off;
-  off += align256(sizeof(double) * kMonHist);
+  off += align256(sizeof(double) * kMonHist * mon_width(system));
   // BSSN: HBM derivative table of the table-fission kernels, [slot][interior point]
   p.tab = off;
   if (system == CHEMORA_SYS_BSSN) off += align256(sizeof(double) * (size_t)kBssnTab * L.nx * L.ny * L.nz);
@@ -721,6 +725,45 @@ int chemora_rhs(chemora_grid_t g, double* dst, void* stream) {
   return CHEMORA_OK;
 }
 
+// Fused monitors: wave -- the energy of the new state, reduced by the
+// kernel that writes it (launch slot `state_slot`); BSSN -- the constraint partials of the state
+// entering the step, reduced by the stage-1 kernel of the fused design (variant 4) with no extra
+// pass over the state, or (other designs) by the constraint kernel before stage 1.
+bool monitor_on(chemora_grid_t g) { return g->monitor && g->mon_n > 0; }
+double* mon_entry(chemora_grid_t g) {
+  return g->mon_hist + (g->mon_written % kMonHist) * (uint64_t)mon_width(g->desc.system);
+}
+cudaError_t mon_begin(chemora_grid_t g, StageLaunch& a, bool state_launch, int stage, cudaStream_t st) {
+  if (!monitor_on(g)) return cudaSuccess;
+  if (g->desc.system == CHEMORA_SYS_WAVE) {
+    if (!state_launch) return cudaSuccess;
+    a.mon_partials = g->mon_partials;
+    return cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st);
+  }
+  if (stage != 1) return cudaSuccess;
+  if (g->variant == 4) {
+    a.mon_partials = g->mon_partials;
+    return cudaSuccess;
+  }
+  StageLaunch c = a;  // the state entering the step is y
+  return bssn_constraints(c, nullptr, g->norm_scratch, mon_entry(g), st);
+}
+cudaError_t mon_end(chemora_grid_t g, const StageLaunch& a, bool state_launch, int stage, cudaStream_t st) {
+  if (!monitor_on(g)) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (g->desc.system == CHEMORA_SYS_WAVE) {
+    if (!state_launch) return cudaSuccess;
+    const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
+    e = monitor_reduce(g->mon_partials, g->mon_n, vol, mon_entry(g), st);
+  } else {
+    if (stage != 1) return cudaSuccess;
+    if (g->variant == 4) e = bssn_constraints_reduce(g->mon_partials, bssn_fused_grid(g->L, a.k_end - a.k_begin),
+                                                     mon_entry(g), st);
+  }
+  g->mon_written += 1;
+  return e;
+}
+
 int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) {
   if (int rc = check_grid(g)) return rc;
   if (nsteps < 0 || !std::isfinite(dt)) return fail(CHEMORA_E_INVALID, "bad dt or nsteps");
@@ -730,24 +773,16 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
     return fail(CHEMORA_E_PEER, "locally connected slabs step through chemora_rk4_step_multi");
   DeviceGuard dg(g->desc.device);
   cudaStream_t st = as_stream(stream);
-  const bool mon = g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0;
-  const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
   if (use_fused(g)) {
     for (int n = 0; n < nsteps; ++n) {
       StageLaunch a = stage_args(g, dt);
       for (int pair = 0; pair < 2; ++pair) {
         if (int rc = phase_wait(g, st)) return rc;
-        if (pair == 1 && mon) {
-          CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
-          a.mon_partials = g->mon_partials;
-        }
+        CUDA_TRY(mon_begin(g, a, pair == 1, 0, st));
         CUDA_TRY(tmark(g, pair, true, st));
         CUDA_TRY(fused_pair(g->variant, a, pair, st));
         CUDA_TRY(tmark(g, pair, false, st));
-        if (pair == 1 && mon) {
-          CUDA_TRY(monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st));
-          g->mon_written += 1;
-        }
+        CUDA_TRY(mon_end(g, a, pair == 1, 0, st));
         if (int rc = phase_signal(g, st)) return rc;
       }
       swap_state(g);
@@ -759,17 +794,12 @@ int chemora_rk4_step(chemora_grid_t g, double dt, int32_t nsteps, void* stream) 
     StageLaunch a = stage_args(g, dt);
     for (int s = 1; s <= 4; ++s) {
       if (int rc = phase_wait(g, st)) return rc;
-      if (s == 4 && mon) {
-        CUDA_TRY(cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st));
-        a.mon_partials = g->mon_partials;
-      }
+      a.mon_partials = nullptr;
+      CUDA_TRY(mon_begin(g, a, s == 4, s, st));
       CUDA_TRY(tmark(g, s - 1, true, st));
       CUDA_TRY(launch_stage(g, a, s, st));
       CUDA_TRY(tmark(g, s - 1, false, st));
-      if (s == 4 && mon) {
-        CUDA_TRY(monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st));
-        g->mon_written += 1;
-      }
+      CUDA_TRY(mon_end(g, a, s == 4, s, st));
       if (int rc = phase_signal(g, st)) return rc;
     }
     g->step += 1;
@@ -871,71 +901,97 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
 
 int chemora_set_monitor(chemora_grid_t g, int enable) {
   if (int rc = check_grid(g)) return rc;
-  if (enable && g->desc.system != CHEMORA_SYS_WAVE)
-    return fail(CHEMORA_E_UNSUPPORTED, "the fused energy monitor is defined for the wave system");
   g->monitor = enable != 0;
   return CHEMORA_OK;
 }
 
 // This slab's per-step energies since the last read (no collective).
+// This slab's raw per-step monitor entries since the last read (no collective): W doubles per
+// step (wave: the energy h^3 sum eps; BSSN: [sum c_q^2, max |c_q|] x 7 of the local slab).
 static int read_monitor_local(chemora_grid_t g, double* out, int32_t max, int32_t* count, cudaStream_t st) {
   if (int rc = check_grid(g)) return rc;
   if (!count || (max > 0 && !out)) return fail(CHEMORA_E_INVALID, "bad output buffer");
   DeviceGuard dg(g->desc.device);
   CUDA_TRY(cudaStreamSynchronize(st));
+  const int W = mon_width(g->desc.system);
   const uint64_t avail = g->mon_written - g->mon_read;
   if (avail > (uint64_t)kMonHist)
     return fail(CHEMORA_E_INVALID, "monitor ring overflowed: read at least every 1024 steps");
   const int32_t n = (int32_t)(avail < (uint64_t)max ? avail : (uint64_t)(max > 0 ? max : 0));
-  std::vector<double> ring(kMonHist);
-  CUDA_TRY(cudaMemcpy(ring.data(), g->mon_hist, sizeof(double) * kMonHist, cudaMemcpyDeviceToHost));
-  for (int32_t i = 0; i < n; ++i) out[i] = ring[(g->mon_read + i) % kMonHist];
+  std::vector<double> ring((size_t)kMonHist * W);
+  CUDA_TRY(cudaMemcpy(ring.data(), g->mon_hist, sizeof(double) * ring.size(), cudaMemcpyDeviceToHost));
+  for (int32_t i = 0; i < n; ++i)
+    for (int w = 0; w < W; ++w) out[(size_t)i * W + w] = ring[((g->mon_read + i) % kMonHist) * W + w];
   g->mon_read += n;
   *count = n;
   return read_nan_flag(g, st);
+}
+
+// Combine per-slab raw entries (rows r = 0..P-1 of n x W, slab order) into global values: sums
+// (wave energy, BSSN sum c^2) added in slab order, maxima; then BSSN L2 = sqrt(h^3 sum).
+static void combine_monitor(const chemora_grid_desc& d, const double* rows, int P, int32_t n, double* out) {
+  const int W = mon_width(d.system);
+  const double vol = d.spacing[0] * d.spacing[1] * d.spacing[2];
+  for (int32_t i = 0; i < n; ++i)
+    for (int w = 0; w < W; ++w) {
+      const bool is_max = W > 1 && (w & 1);
+      double acc = 0.0;
+      for (int r = 0; r < P; ++r) {
+        const double x = rows[((size_t)r * n + i) * W + w];
+        acc = is_max ? std::fmax(acc, x) : acc + x;
+      }
+      out[(size_t)i * W + w] = (W > 1 && !is_max) ? std::sqrt(vol * acc) : acc;
+    }
 }
 
 int chemora_read_monitor(chemora_grid_t g, double* out, int32_t max, int32_t* count, void* stream) {
   if (int rc = check_grid(g)) return rc;
   const int P = g->desc.nranks;
   if (P > 1 && !g->ipc)
-    return fail(CHEMORA_E_PEER, "same-process slabs: read the global energies with chemora_read_monitor_multi");
+    return fail(CHEMORA_E_PEER, "same-process slabs: read the global values with chemora_read_monitor_multi");
   cudaStream_t st = as_stream(stream);
-  int rc = read_monitor_local(g, out, max, count, st);
+  const int W = mon_width(g->desc.system);
+  std::vector<double> mine((size_t)(max > 0 ? max : 1) * W);
+  int rc = read_monitor_local(g, mine.data(), max, count, st);
   if (rc && rc != CHEMORA_E_NONFINITE) return rc;
   const int32_t n = *count;
+  const std::string nonfinite = rc ? g_err : std::string();
   if (P > 1 && n > 0) {
-    // collective: the global energy of each step is the sum of the slabs' values, added in
-    // rank order (every rank gets the same values; ranks step in lockstep, so n agrees)
-    const std::string nonfinite = rc ? g_err : std::string();
-    std::vector<double> all((size_t)n * P);
+    // collective: every rank gets the same global values (ranks step in lockstep, so n agrees)
+    if ((size_t)n * W > (size_t)kGatherLen) return fail(CHEMORA_E_INVALID, "read the monitor more often");
+    std::vector<double> all((size_t)n * W * P);
     DeviceGuard dg(g->desc.device);
-    if (int rc1 = ring_allgather(g, out, n, all.data(), st)) return rc1;
-    for (int32_t i = 0; i < n; ++i) {
-      double s = 0.0;
-      for (int r = 0; r < P; ++r) s += all[(size_t)r * n + i];
-      out[i] = s;
-    }
-    if (rc) g_err = nonfinite;
+    if (int rc1 = ring_allgather(g, mine.data(), n * W, all.data(), st)) return rc1;
+    combine_monitor(g->desc, all.data(), P, n, out);
+  } else if (n > 0) {
+    combine_monitor(g->desc, mine.data(), 1, n, out);
   }
+  if (rc) g_err = nonfinite;
   return rc;
 }
 
 int chemora_read_monitor_multi(chemora_grid_t* grids, int32_t n, double* out, int32_t max, int32_t* count,
                                void* stream) {
   if (!grids || n < 1 || !count || (max > 0 && !out)) return fail(CHEMORA_E_INVALID, "bad arguments");
-  std::vector<double> part((size_t)(max > 0 ? max : 1));
+  if (int rc = check_grid(grids[0])) return rc;
+  const int W = mon_width(grids[0]->desc.system);
+  const size_t cap = (size_t)(max > 0 ? max : 1) * W;
+  std::vector<double> rows(cap * n);
   int32_t cnt0 = -1;
   int status = CHEMORA_OK;
   for (int r = 0; r < n; ++r) {
     int32_t c = 0;
-    int rc = read_monitor_local(grids[r], part.data(), max, &c, as_stream(stream));
+    int rc = read_monitor_local(grids[r], rows.data() + cap * r, max, &c, as_stream(stream));
     if (rc && rc != CHEMORA_E_NONFINITE) return rc;
     if (rc) status = rc;
     if (cnt0 >= 0 && c != cnt0) return fail(CHEMORA_E_PEER, "slabs recorded different step counts");
-    for (int32_t i = 0; i < c; ++i) out[i] = (r == 0 ? 0.0 : out[i]) + part[i];  // slab order
     cnt0 = c;
   }
+  // rows were written with stride cap; compact to n x (cnt0 x W) in slab order
+  std::vector<double> packed((size_t)n * cnt0 * W);
+  for (int r = 0; r < n; ++r)
+    for (size_t q = 0; q < (size_t)cnt0 * W; ++q) packed[(size_t)r * cnt0 * W + q] = rows[cap * r + q];
+  if (cnt0 > 0) combine_monitor(grids[0]->desc, packed.data(), n, cnt0, out);
   *count = cnt0;
   return status;
 }
@@ -979,38 +1035,24 @@ int chemora_rk4_step_multi(chemora_grid_t* grids, int32_t n, double dt, int32_t 
   cudaStream_t st = as_stream(stream);
   bool fused = true;
   for (int r = 0; r < n; ++r) fused = fused && use_fused(grids[r]);
-  // per-slab fused energy monitor: the kernel that writes the new state leaves its partials,
-  // reduced into that slab's history (the global energy is the sum over slabs)
-  auto mon_on = [&](chemora_grid_t g) { return g->monitor && g->desc.system == CHEMORA_SYS_WAVE && g->mon_n > 0; };
-  auto mon_begin = [&](chemora_grid_t g, StageLaunch& a) -> cudaError_t {
-    if (!mon_on(g)) return cudaSuccess;
-    a.mon_partials = g->mon_partials;
-    return cudaMemsetAsync(g->mon_partials, 0, sizeof(double) * g->mon_n, st);
-  };
-  auto mon_end = [&](chemora_grid_t g) -> cudaError_t {
-    if (!mon_on(g)) return cudaSuccess;
-    const double vol = g->desc.spacing[0] * g->desc.spacing[1] * g->desc.spacing[2];
-    cudaError_t e = monitor_reduce(g->mon_partials, g->mon_n, vol, g->mon_hist + g->mon_written % kMonHist, st);
-    g->mon_written += 1;
-    return e;
-  };
+  // per-slab fused monitors (the global values combine the slabs', chemora_read_monitor_multi)
   for (int step = 0; step < nsteps; ++step) {
     if (fused) {
       for (int pair = 0; pair < 2; ++pair)
         for (int r = 0; r < n; ++r) {
           StageLaunch a = stage_args(grids[r], dt);
-          if (pair == 1) CUDA_TRY(mon_begin(grids[r], a));
+          CUDA_TRY(mon_begin(grids[r], a, pair == 1, 0, st));
           CUDA_TRY(fused_pair(grids[r]->variant, a, pair, st));
-          if (pair == 1) CUDA_TRY(mon_end(grids[r]));
+          CUDA_TRY(mon_end(grids[r], a, pair == 1, 0, st));
         }
       for (int r = 0; r < n; ++r) swap_state(grids[r]);
     } else {
       for (int s = 1; s <= 4; ++s)
         for (int r = 0; r < n; ++r) {
           StageLaunch a = stage_args(grids[r], dt);
-          if (s == 4) CUDA_TRY(mon_begin(grids[r], a));
+          CUDA_TRY(mon_begin(grids[r], a, s == 4, s, st));
           CUDA_TRY(launch_stage(grids[r], a, s, st));
-          if (s == 4) CUDA_TRY(mon_end(grids[r]));
+          CUDA_TRY(mon_end(grids[r], a, s == 4, s, st));
         }
     }
     for (int r = 0; r < n; ++r) grids[r]->step += 1;

@@ -261,6 +261,13 @@ cudaError_t ghost_fill(const Layout& L, double* set, FaceDst z, cudaStream_t st)
   return cudaGetLastError();
 }
 
+cudaError_t push_z_planes(const Layout& L, const double* set, FaceDst z, cudaStream_t st) {
+  const int T = 256;
+  const int64_t n = (L.nx + 2 * L.g) * (L.ny + 2 * L.g) * L.g;
+  push_z<<<dim3((unsigned)((n + T - 1) / T), L.n_gf), T, 0, st>>>(L, set, z.lo, z.hi);
+  return cudaGetLastError();
+}
+
 cudaError_t init_interior(const Layout& L, double* set, const InitArgs& a, cudaStream_t st) {
   dim3 block(128);
   dim3 grid((unsigned)((L.nx + 127) / 128), (unsigned)L.ny, (unsigned)L.nz);

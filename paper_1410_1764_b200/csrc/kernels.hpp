@@ -57,6 +57,11 @@ cudaError_t bssn_rhs(const StageLaunch& a, double* dst, cudaStream_t st);
 // variant 4 (bssn_fused.cu): one fused kernel per stage, derivatives on chip (SMEM plane tiles
 // + TMEM z-windows); stage 0 = RHS only into dst
 cudaError_t bssn_fused_stage(const StageLaunch& a, int stage, double* dst, cudaStream_t st);
+// CTAs of a bssn_fused launch over nk planes (stage 1 with a.mon_partials set leaves 14
+// partials [sum c_q^2, max|c_q|] per CTA: the fused constraint monitor)
+int bssn_fused_grid(const Layout& L, int nk);
+// fixed-order combination of nblocks x 14 constraint partials into out14 (device)
+cudaError_t bssn_constraints_reduce(const double* part, int nblocks, double* out14, cudaStream_t st);
 // BSSN constraints H, M^i, G^i of a.s.y (R16): optional interior fields
 // [7][z][y][x] (nullable) and, on the device, out_dev[2q] = sum c_q^2, out_dev[2q+1] =
 // max |c_q| (scratch: kNormBlocks x 14 doubles).
@@ -65,6 +70,10 @@ cudaError_t bssn_constraints(const StageLaunch& a, double* fields, double* scrat
 
 // Ghost fill of one set (all GFs): x and y locally, then z images stored to face bases.
 cudaError_t ghost_fill(const Layout& L, double* set, FaceDst z, cudaStream_t st);
+
+// z ghost planes only: this slab's first/last g planes (x/y ghosts included) into the lo/hi
+// faces (the neighbours' copies of the same set, or our own for a whole-z grid).
+cudaError_t push_z_planes(const Layout& L, const double* set, FaceDst z, cudaStream_t st);
 
 // Device initial data into the interior of set y (global coordinates).
 struct InitArgs {

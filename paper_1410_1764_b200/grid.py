@@ -121,8 +121,11 @@ class Grid:
         C.chemora_set_monitor(self.handle, enable)
 
     def read_monitor(self, max_steps=1024):
-        """Per-step energies since the last read (global values, collective when nranks > 1)."""
-        return C.chemora_read_monitor(self.handle, max_steps, self.stream)
+        """Per-step monitor values since the last read (global values, collective when
+        nranks > 1): wave -- the energy after each step, shape (n,); BSSN -- [L2, Linf] of
+        H, M1..3, G1..3 of the state entering each step, shape (n, 14)."""
+        w = 14 if self.system == C.SYS_BSSN else 1
+        return C.chemora_read_monitor(self.handle, max_steps, self.stream, w)
 
     def autotune(self, trials=3):
         return C.chemora_autotune(self.handle, trials, self.stream)
@@ -184,7 +187,8 @@ class LocalSlabs:
 
     def read_monitor(self, max_steps=1024):
         """Per-step global energies: the slabs' fused-monitor values summed in slab order."""
-        return C.chemora_read_monitor_multi(self.handles, max_steps, self.stream)
+        w = 14 if self.grids[0].system == C.SYS_BSSN else 1
+        return C.chemora_read_monitor_multi(self.handles, max_steps, self.stream, w)
 
     def close(self):
         for g in self.grids:

@@ -53,7 +53,7 @@ def run(rank, world, port, case, q):
         out["pad"] = g.get_state(padded=True)
         out["norms"] = g.norms()
         if case.get("monitor"):
-            out["energy"] = g.read_monitor()
+            out["monitor"] = g.read_monitor()
         if system == C.SYS_BSSN:
             out["cnorms"] = g.constraint_norms()
         torch.cuda.synchronize()

@@ -121,12 +121,18 @@ def _check(world, case, tol):
         assert np.array_equal(r["norms"], res[0]["norms"])
     onorm = oracle.norms(sysid, ref, h)
     np.testing.assert_allclose(res[0]["norms"], onorm, rtol=1e-11, atol=1e-13 * np.abs(onorm).max())
-    if "energy" in res[0]:
-        e = res[0]["energy"]
+    if "monitor" in res[0]:
+        e = res[0]["monitor"]
         assert len(e) == case["steps"]
         for r in res[1:]:
-            assert np.array_equal(r["energy"], e)
-        assert e[-1] == pytest.approx(onorm[-1], rel=1e-12)
+            assert np.array_equal(r["monitor"], e)
+        if case["system"] == "wave":   # energy after the last step
+            assert e[-1] == pytest.approx(onorm[-1], rel=1e-12)
+        else:                          # constraint norms of the state entering step 1
+            c = oracle.constraints(y0, h)
+            vol = h[0] * h[1] * h[2]
+            oc = np.array([[math.sqrt(vol * (c[q] ** 2).sum()), np.abs(c[q]).max()] for q in range(7)]).ravel()
+            np.testing.assert_allclose(e[0], oc, rtol=1e-10, atol=1e-10 * np.abs(oc).max())
     if "cnorms" in res[0]:
         for r in res[1:]:
             assert np.array_equal(r["cnorms"], res[0]["cnorms"])
@@ -146,7 +152,8 @@ def test_wave_ipc_processes(world, variant, init):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_bssn_ipc_processes(world):
+@pytest.mark.parametrize("variant", [3, 4])
+def test_bssn_ipc_processes(world, variant):
     case = {"system": "bssn", "n": (20, 16, 36), "L": 1.0, "init": "host", "seed": 1410,
-            "eps": 1e-2, "steps": 2, "params": GENERIC}
+            "eps": 1e-2, "steps": 2, "params": GENERIC, "variant": variant, "monitor": True}
     _check(world, case, 1e-10)

@@ -121,3 +121,37 @@ def test_energy_monitor_local_slabs(nslabs, variant):
     ref.set_initial(C.INIT_HOST, y0)
     ref.rk4_step(dt, 3)
     assert np.array_equal(s.get_state(), ref.get_state())
+
+
+@pytest.mark.parametrize("variant", [4, 3])
+def test_bssn_constraint_monitor_matches_oracle(variant):
+    """NEXT-3 for BSSN: with the monitor on, every step's stage-1 kernel
+    reduces [L2, Linf] of H, M^i, G^i of the state entering the step (design 4: fused, from the
+    on-chip derivatives; design 3: the constraint kernel before stage 1).  Equal to the oracle's
+    constraints of the oracle's state after s = 0, 1, 2 steps (1e-10 of each norm, R11), and
+    the monitored step is bitwise the unmonitored one."""
+    P, C = _mods()
+    n = (28, 20, 24)
+    h = tuple(1.0 / v for v in n)
+    dt = 0.25 * min(h)
+    y0 = ci.mink_pert(n, h, 1410, eps=1e-2)
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_kernel_variant(variant)
+    g.set_initial(C.INIT_HOST, y0)
+    g.set_monitor(True)
+    g.rk4_step(dt, 3)
+    m = g.read_monitor()
+    assert m.shape == (3, 14)
+    vol = h[0] * h[1] * h[2]
+    y = y0
+    for s in range(3):
+        c = oracle.constraints(y, h)
+        ref = np.array([[math.sqrt(vol * (c[q] ** 2).sum()), np.abs(c[q]).max()] for q in range(7)]).ravel()
+        np.testing.assert_allclose(m[s], ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())
+        y = oracle.rk4(oracle.BSSN, y, h, dt, 1)
+    r = P.Grid(C.SYS_BSSN, n, h)
+    r.set_kernel_variant(variant)
+    r.set_initial(C.INIT_HOST, y0)
+    r.rk4_step(dt, 3)
+    assert np.array_equal(r.get_state(), g.get_state())
+    assert len(g.read_monitor()) == 0
