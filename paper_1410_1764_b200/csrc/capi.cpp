@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys timelines (no-ops without a tool)
+
 #include "grid.hpp"
 #include "kernels.hpp"
 
@@ -271,6 +273,8 @@ int load_stream_memops() {
 
 int phase_wait(chemora_grid_t g, cudaStream_t st) {
   if (!g->ipc || g->epoch == 0) return CHEMORA_OK;
+  nvtxRangePushA("chemora phase wait");
+  struct Pop { ~Pop() { nvtxRangePop(); } } pop;
   if (int rc = load_stream_memops()) return rc;
   const uint64_t want = g->epoch;  // neighbours completed phase `epoch`
   for (int f = 0; f < 2; ++f) {
@@ -306,6 +310,8 @@ int phase_signal(chemora_grid_t g, cudaStream_t st) {
 // that follows is deterministic and identical everywhere.  Synchronises the stream.
 int ring_allgather(chemora_grid_t g, const double* host_src, int len, double* host_out, cudaStream_t st) {
   const int P = g->desc.nranks, r = g->desc.rank;
+  nvtxRangePushA("chemora ring allgather");
+  struct Pop { ~Pop() { nvtxRangePop(); } } pop;
   if (len > kGatherLen) return fail(CHEMORA_E_INVALID, "gather length too large");
   if (P == 1) {
     memcpy(host_out, host_src, sizeof(double) * len);
@@ -334,7 +340,12 @@ int ring_allgather(chemora_grid_t g, const double* host_src, int len, double* ho
 // a step (slot = which launch of the step: wave pair A/B = 0/1, else RK stage 1..4 = 0..3).
 constexpr size_t kMaxTimed = 4096;
 constexpr int kTimingSlots = 8;
+// NVTX range names per launch slot (host-side enqueue of each phase of the step)
+const char* const kPhaseName[2][4] = {{"chemora stage 1", "chemora stage 2", "chemora stage 3", "chemora stage 4"},
+                                      {"chemora stages 1+2", "chemora stages 3+4", "", ""}};
 cudaError_t tmark(chemora_grid_t g, int slot, bool begin, cudaStream_t st) {
+  if (begin) nvtxRangePushA(kPhaseName[g->variant == 8 && g->desc.system == CHEMORA_SYS_WAVE][slot & 3]);
+  else nvtxRangePop();
   if (!g->timing) return cudaSuccess;
   if (begin) {
     if (g->tn >= kMaxTimed) return cudaSuccess;  // full: later launches are not timed

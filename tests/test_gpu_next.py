@@ -60,13 +60,6 @@ def test_fused_energy_monitor_matches_oracle(n, variant):
     assert np.array_equal(g.read_monitor(), e)
 
 
-def test_monitor_rejects_bssn():
-    P, C = _mods()
-    g = P.Grid(C.SYS_BSSN, (16, 16, 16), (1 / 16,) * 3)
-    with pytest.raises(C.ChemoraError):
-        g.set_monitor(True)
-
-
 @pytest.mark.parametrize("system", ["wave", "bssn"])
 def test_autotune_keeps_state_and_parity(system):
     """The autotuner times stage-1 launches with dt = 0 (state untouched) and keeps the
