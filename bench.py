@@ -418,7 +418,9 @@ def main():
                 roofline["peak_measured_burst"] = meas["burst"]
                 roofline["frac_of_measured_sustained"] = achieved / meas["sustained"]
         per_slot_ms = {f"slot{s}": {"avg_ms": avg[s], "launches": counts[s]} for s in slots}
-        kernels_per_slot = 3 if (system == C.SYS_BSSN and variant in (2, 3)) else 1
+        # BSSN: 3 kernels per stage for designs 2/3 (fission), 2 for design 4 (the fused
+        # stage kernel + the z ghost-plane push)
+        kernels_per_slot = (3 if variant in (2, 3) else 2 if variant == 4 else 1) if system == C.SYS_BSSN else 1
         launches = kernels_per_slot * sum(counts[s] for s in slots)
 
         e2e = None

@@ -308,8 +308,9 @@ int chemora_read_launch_timing(chemora_grid_t grid, double* ms_sum, int32_t* cou
  * RK stage), 6 = temporally blocked stage pairs on 32x8 tiles, 7 = the same on 32x16 tiles,
  * 8 = 6 with register-queue z stencils (default for 4th order; 6-8 are 4th order only);
  * every wave design is bitwise identical.  BSSN: 0 =
- * two-phase SMEM table, 1 = fused single kernel, 2 = fissioned G1/G2/G3, 3 = HBM derivative
- * table + algebra kernels (default); results agree to rounding. */
+ * two-phase SMEM table, 2 = fissioned G1/G2/G3, 3 = HBM derivative table + algebra kernels,
+ * 4 = one fused kernel per stage with the derivatives on chip (SMEM plane tiles by TMA, TMEM
+ * z-windows; default); results agree to rounding.  Refused after chemora_grid_connect_ipc. */
 int chemora_set_kernel_variant(chemora_grid_t grid, int variant);
 
 /* The kernel design chemora_rk4_step will run for this handle (a temporally blocked variant

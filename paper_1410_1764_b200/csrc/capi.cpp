@@ -532,12 +532,13 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   // 4th-order wave grids (variant 8, fastest measured, profiles/r1_wave_design_study.md);
   // orders 6/8: the persistent TMA z-march when its 32x16 tiles fill the SMs (variant 4:
   // 14.2 vs 15.6-18.1 ms/step at 512^3, profiles/r1_fd_orders.jsonl), else one thread per
-  // point (also for order 2, where it is fastest); BSSN: fission at the derivative/algebra
-  // boundary through the HBM table (fastest measured at 192^3)
+  // point (also for order 2, where it is fastest); BSSN: the fused per-stage kernel with the
+  // derivatives on chip (variant 4: as fast as the HBM-table fission, variant 3, at 192^3 with
+  // a fifth of its DRAM traffic, profiles/r2_bssn_summary.md)
   {
     const int order = desc->fd_order == 0 ? 4 : desc->fd_order;
     const int64_t tiles16 = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
-    g->variant = desc->system == CHEMORA_SYS_BSSN ? 3 /* HBM derivative table */
+    g->variant = desc->system == CHEMORA_SYS_BSSN ? 4 /* fused, SMEM tiles + TMEM z-windows */
                : order == 4 ? kVariantFused3 : (order >= 6 && tiles16 >= 148) ? 4 : 0;
   }
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
@@ -849,6 +850,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     cands.push_back({0, 0});
     cands.push_back({2, 0});  // fissioned one-thread-per-point kernels
     cands.push_back({3, 0});  // HBM derivative table + algebra kernels
+    cands.push_back({4, 0});  // fused: SMEM plane tiles + TMEM z-windows
   }
   const int saved_v = g->variant, saved_b = g->band;
   cudaEvent_t e0, e1, e2;
