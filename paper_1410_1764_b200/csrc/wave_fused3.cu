@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(NT, 1)
   const double C1W = D1W<W>::c(1), C2W = D1W<W>::c(2);
 
   double eacc = 0.0;  // this thread's energy sum (B, monitor on), in a fixed point order
+  uint32_t bad = 0;   // B: bit f set once GF f produced a non-finite value (reported at the end)
   uint32_t nz = 0, np = 0, nq = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
@@ -385,12 +386,12 @@ __global__ void __launch_bounds__(NT, 1)
           } else {
             double* outy = a.s.b;  // the new state goes to the scratch set (swapped by the caller)
             const FaceDst fd = a.img[0];
-            const unsigned long long code0 = a.step * (unsigned long long)L.n_gf;
             double esq = 0.0;  // rho^2 + v.v of the new state (fused energy monitor)
             auto put = [&](int f, double v) {
               outy[f * gfs + c] = v;
               put_images(isite, outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
-              check_finite(a.nan_flag, code0 + f, v);
+              // branch-free non-finite check (NaN and +-Inf fail |v| <= DBL_MAX)
+              bad |= (fabs(v) <= 1.7976931348623157e308 ? 0u : 1u) << f;
               if (f >= 1) esq += v * v;
             };
             auto putq = [&](int, double) {};
@@ -439,6 +440,9 @@ __global__ void __launch_bounds__(NT, 1)
     nz = z0 + nk + 8;
     np = p0 + nk + 4;
   }
+  // the first non-finite GF of this thread (the flag keeps min(step * n_gf + gf) over threads)
+  if (B && bad) check_finite(a.nan_flag, a.step * (unsigned long long)a.L.n_gf + (unsigned long long)(__ffs(bad) - 1),
+                             __longlong_as_double(0x7ff8000000000000ll));
   // NEXT-3 fused energy monitor (Fig. 1 "Energy"): one partial per CTA,
   // fixed shuffle tree then warps in order, so the per-step energy is deterministic
   if (B && a.mon_partials) {
