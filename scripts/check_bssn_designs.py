@@ -1,4 +1,4 @@
-"""Bring-up check of BSSN variant 4 on small grids: RHS and one step vs variant 3."""
+"""BSSN designs 3 (HBM table) and 4 (fused, on-chip derivatives) on small ragged grids: RHS and one step agree to rounding."""
 import faulthandler, sys, math
 faulthandler.enable()
 sys.path.insert(0, ".")
