@@ -631,6 +631,7 @@ __device__ __forceinline__ void bssn_update_src(const StageLaunch& a, const Bssn
   // pointers), so loads interleaved with the stores would serialise one memory round trip
   // per GF
   double p0[NV], p1[NV];
+  uint32_t bad = 0;  // bit v: GF v non-finite (branch-free check, one report per point)
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (!in_group(G, v)) continue;
@@ -661,8 +662,9 @@ __device__ __forceinline__ void bssn_update_src(const StageLaunch& a, const Bssn
     } else {
       put_images(isite, out + v * gfs, fd.lo + v * gfs, fd.hi + v * gfs, L, i, j, k, c, val);
     }
-    if (STAGE == 4) check_finite(a.nan_flag, code0 + v, val);
+    if (STAGE == 4) bad |= (fabs(val) <= 1.7976931348623157e308 ? 0u : 1u) << v;
   }
+  if (STAGE == 4 && bad) atomicMin(a.nan_flag, code0 + (unsigned long long)(__ffs(bad) - 1));
 }
 
 template <int STAGE>
