@@ -48,3 +48,25 @@ def test_variant_parity(variant, params):
     got = g.get_state()
     assert relerr(got, ref) <= 1e-10
     assert relerr(got - y0, ref - y0) <= 1e-8
+
+
+@pytest.mark.parametrize("variant", [3, 4])
+def test_nonfinite_reported_with_gf(variant):
+    """A NaN injected into one GF (gt22) surfaces as CHEMORA_E_NONFINITE at the next
+    synchronising call, naming the first offending GF and the step."""
+    P, C = _mods()
+    n = (16, 16, 16)
+    h = tuple(1.0 / v for v in n)
+    y0 = ci.mink_pert(n, h, 1410, eps=1e-3)
+    y0[ci.BSSN_GF.index("gt22"), 3, 4, 5] = np.nan
+    g = P.Grid(C.SYS_BSSN, n, h)
+    g.set_kernel_variant(variant)
+    g.set_initial(C.INIT_HOST, y0)
+    g.rk4_step(0.25 * min(h), 1)
+    with pytest.raises(C.ChemoraError) as ei:
+        g.get_state()
+    assert ei.value.code == C.E_NONFINITE
+    msg = str(ei.value)
+    assert "at step 0" in msg
+    # the NaN spreads to every GF through the stencils; the flag keeps the lowest index
+    assert "grid function 0" in msg
