@@ -194,6 +194,8 @@ def test_local_slabs_bitwise_bssn():
     s.set_initial(C.INIT_HOST, y0)
     s.rk4_step(dt, 3)
     assert np.array_equal(s.get_state(), g.get_state())
+    # ... and element-wise against the oracle
+    assert relerr(s.get_state(), oracle.rk4(B, y0, h, dt, 3, BENCH)) <= 1e-10
 
 
 def test_full_size_192_sampled_parity():

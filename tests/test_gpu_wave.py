@@ -157,6 +157,9 @@ def test_local_slabs_bitwise_equal_single_grid(nslabs):
     s.rk4_step(0.25 * min(h), 5)
     assert np.array_equal(s.get_state(), ref)
     np.testing.assert_allclose(s.norms(), g.norms(), rtol=1e-14)
+    # ... and element-wise against the oracle (not only against the GPU's own single grid)
+    o = oracle.rk4(W, y0, h, 0.25 * min(h), 5)
+    assert max(np.abs(s.get_state()[f] - o[f]).max() / np.abs(o[f]).max() for f in range(5)) <= 1e-12
     # ghosts of every slab are the periodic images of the global state
     full = np.pad(ref, ((0, 0), (3, 3), (3, 3), (3, 3)), mode="wrap")
     for gg, pad in zip(s.grids, s.get_state_padded()):
