@@ -53,7 +53,11 @@ constexpr int FPLS = (FPL * 8 + 127) / 128 * 16;       // GF plane stride in the
 constexpr int TILE_STRIDE = (NV * FPLS * 8 + 1023) / 1024 * 1024;
 constexpr int GZX_N = NMIX * FY * HXW, GZY_N = NMIX * HYH * FX, GYX_N = NMIX * FY * HXW;
 constexpr int NMON = 14;                               // constraint monitor: [sum c_q^2, max|c_q|] x 7
-constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64 + 8 * NWARP * NMON;
+// the own-column feed of plane k+3: the tile interior of that plane, one TMA box (16, 8) per GF,
+// streamed in one iteration ahead into a double buffer
+constexpr int FEED_PL = FPT;                            // doubles per GF (1 KB)
+constexpr int FEED_STRIDE = NV * FEED_PL * 8;           // bytes per buffer (25.6 KB)
+constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 2 * FEED_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64 + 8 * NWARP * NMON;
 // TMEM window feed split over the groups: [0, 9) [9, 17) [17, 25) (3 groups) or [0, 13) [13, 25)
 // -- the 11 GFs with mixed derivatives stay with one group each (phi, gt: 0; alpha, beta: last)
 constexpr int FEED_B1 = NGRP == 3 ? 9 : 13, FEED_B2 = NGRP == 3 ? 17 : 25;
@@ -177,22 +181,27 @@ struct TileIn {
 };
 
 struct FusedMaps {
-  CUtensorMap in;  // the stage input set, box (FSX, FSY, 1, NV)
+  CUtensorMap in;    // the stage input set, box (FSX, FSY, 1, 1)
+  CUtensorMap feed;  // the same set, box (FX, FY, 1, 1): the tile interior (the TMEM feed)
 };
 
-template <int STAGE>
+// MON: the stage-1 instantiation with the fused constraint monitor (a separate kernel, so the
+// default one carries neither its code nor its registers)
+template <int STAGE, bool MON>
 __global__ void __launch_bounds__(FNT, 1)
     bssn_fused(const __grid_constant__ FusedMaps M, StageLaunch a, BssnK K, int ntx, int nty, int chunk,
                int nitems, double* rhs_dst) {
   extern __shared__ __align__(1024) unsigned char smem[];
   double* tiles = reinterpret_cast<double*>(smem);                       // 2 x TILE_STRIDE bytes
-  double* gzx = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE);
+  double* feeds = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE);      // 2 x FEED_STRIDE bytes
+  double* gzx = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE + 2 * FEED_STRIDE);
   double* gzy = gzx + GZX_N;
   double* gyx = gzy + GZY_N;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(gyx + GYX_N);           // 2 mbarriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
-  double* macc = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64);  // [8][NMON]
-  const bool monitor = STAGE == 1 && a.mon_partials != nullptr;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(gyx + GYX_N);           // 2 tile + 2 feed mbarriers
+  uint64_t* fbar = mbar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 4);
+  double* macc = reinterpret_cast<double*>(smem + 2 * TILE_STRIDE + 2 * FEED_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64);
+  constexpr bool monitor = STAGE == 1 && MON;
   const Layout& L = a.L;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = warp >> 2;                     // 0: G2; 1: G13 (2 groups) or G1; 2: G3
@@ -211,10 +220,10 @@ __global__ void __launch_bounds__(FNT, 1)
   if (tid == 0) *tmem_slot = 0;
 #endif
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    for (int q = 0; q < 2; ++q) { mbar_init(&mbar[q], 1); mbar_init(&fbar[q], 1); }
     fence_mbar_init();
     prefetch_tmap(&M.in);
+    prefetch_tmap(&M.feed);
   }
   cta_sync_tm();
   const uint32_t tb = *tmem_slot + ((uint32_t)((warp & 3) * 32) << 16);
@@ -239,6 +248,14 @@ __global__ void __launch_bounds__(FNT, 1)
                   L.g + j0 - FR, L.g + k, q);
 #endif
   };
+  auto issue_feed = [&](int buf, int i0, int j0, int k) {  // tile interior of plane k, all GFs
+    mbar_arrive_expect_tx(&fbar[buf], (uint32_t)FEED_STRIDE);
+#pragma unroll 1
+    for (int q = 0; q < NV; ++q)
+      tma_load_4d(feeds + (size_t)buf * (FEED_STRIDE / 8) + q * FEED_PL, &M.feed, &fbar[buf], kXOff + i0, L.g + j0,
+                  L.g + k, q);
+  };
+  uint32_t fphase = 0;  // parity bit per feed buffer
   const int64_t gfs = L.gfs;
   const int xlo = -L.g, xhi = (int)L.nx + L.g - 1, ylo = -L.g, yhi = (int)L.ny + L.g - 1;
   uint32_t phase = 0;  // parity bit per tile buffer
@@ -247,6 +264,7 @@ __global__ void __launch_bounds__(FNT, 1)
     int i0, j0, kb, ke;
     item_geom(blockIdx.x, i0, j0, kb, ke);
     issue_tile(0, i0, j0, kb);
+    issue_feed(0, i0, j0, kb + 3);
   }
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     int i0, j0, kb, ke;
@@ -290,12 +308,15 @@ __global__ void __launch_bounds__(FNT, 1)
       const int buf = n & 1;
       // ---- next plane's tile (this item's k+1, or the next item's first plane) into the other
       // buffer: its last reader (plane n-1) finished at the end-of-plane barrier
-      if (tid == 0) {
-        if (k + 1 < ke) issue_tile(buf ^ 1, i0, j0, k + 1);
-        else if (it + (int)gridDim.x < nitems) {
+      if (tid == 0) {  // and the next plane's TMEM feed (plane k+4, or the next item's kb+3)
+        if (k + 1 < ke) {
+          issue_tile(buf ^ 1, i0, j0, k + 1);
+          issue_feed(buf ^ 1, i0, j0, k + 4);
+        } else if (it + (int)gridDim.x < nitems) {
           int ni0, nj0, nkb, nke;
           item_geom(it + gridDim.x, ni0, nj0, nkb, nke);
           issue_tile(buf ^ 1, ni0, nj0, nkb);
+          issue_feed(buf ^ 1, ni0, nj0, nkb + 3);
         }
       }
       // ---- all global loads of the plane first (one exposed latency): the D1_z frame operands
@@ -320,18 +341,11 @@ __global__ void __launch_bounds__(FNT, 1)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pre + v * gfs));
       }
       // ... the own column two planes ahead of the feed pulled into L2 (its first touch is
-      // an HBM round trip) ...
+      // an HBM round trip; the feed itself arrives by TMA one plane ahead)
       {
         const int kp = min(k + 5, (int)L.nz + L.g - 1);
         for (int gf = g_lo; gf < g_hi; ++gf)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(col + gf * gfs + (int64_t)kp * L.plane));
-      }
-      // ... and the own-column values of plane k+3 for this thread's GF half (for the shift)
-      double feed[FEEDN];
-#pragma unroll
-      for (int q = 0; q < FEEDN; ++q) {
-        const int gf = g_lo + q;
-        if (gf < g_hi) feed[q] = __ldg(col + gf * gfs + (int64_t)(k + 3) * L.plane);
       }
       mbar_wait(&mbar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
@@ -347,9 +361,13 @@ __global__ void __launch_bounds__(FNT, 1)
 #pragma unroll
       for (int m = 0; m < NFI; ++m)
         if (tid + m * FNT < NMIX * NFRAME) gzx[fdst[m]] = 8.0 * (fv[m][2] - fv[m][1]) - (fv[m][3] - fv[m][0]);
-      // ---- TMEM window shift (planes k-3 .. k+3) with the new plane k+3, and D1raw_z of the
-      // mixed GFs at the own point into the interior of the z helpers.  tcgen05.ld/st are
-      // .sync.aligned: reconverge the warp after the thread-dependent helper loops first
+      // ---- TMEM window shift (planes k-3 .. k+3) with the new plane k+3 (from the TMA feed
+      // buffer), and D1raw_z of the mixed GFs at the own point into the interior of the z
+      // helpers.  tcgen05.ld/st are .sync.aligned: reconverge the warp after the
+      // thread-dependent helper loops first
+      mbar_wait(&fbar[buf], (fphase >> buf) & 1u);
+      fphase ^= 1u << buf;
+      const double* fb = feeds + (size_t)buf * (FEED_STRIDE / 8) + ty * FX + tx;
       __syncwarp();
 #pragma unroll
       for (int q = 0; q < FEEDN; ++q) {
@@ -368,8 +386,9 @@ __global__ void __launch_bounds__(FNT, 1)
         uint32_t w[16];
 #pragma unroll
         for (int s = 0; s < 12; ++s) w[s] = r[s + 2];
-        w[12] = (uint32_t)__double2loint(feed[q]);
-        w[13] = (uint32_t)__double2hiint(feed[q]);
+        const double fv = fb[gf * FEED_PL];
+        w[12] = (uint32_t)__double2loint(fv);
+        w[13] = (uint32_t)__double2hiint(fv);
         w[14] = w[15] = 0u;
         tm_st16(tb + 16u * (uint32_t)gf, w);
       }
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(FNT, 1)
         bssn_point<3>(P, K, r);
         if (live) bssn_update_src<STAGE, 3, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
       }
-      if constexpr (STAGE == 1) {
+      if constexpr (monitor) {
         // NEXT-3 fused constraint monitor: H, M^i, G^i of the state entering
         // this step (stage 1's input, already on chip), reduced per warp in a fixed order
         if (monitor && (grp == 0 || grp == NGRP - 1)) {  // H by the G2 warps, M and G by the last group
@@ -468,13 +487,18 @@ cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cuda
 #endif
   FusedMaps M;
   const double* in = stage_input<STAGE>(a);
-  if (!encode_set_map(&M.in, in - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, FSX, FSY, 1))
+  if (!encode_set_map(&M.in, in - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, FSX, FSY, 1) ||
+      !encode_set_map(&M.feed, in - L.c0, L.px, L.py, L.pz, L.n_gf, L.gfs, FX, FY, 1))
     return cudaErrorInvalidValue;
 #ifdef CHEMORA_DEBUG_FUSED
   fprintf(stderr, "launch_fused<%d> encoded\n", STAGE);
 #endif
-  static std::atomic<uint64_t> attr_done{0};
-  if (cudaError_t e = smem_optin((const void*)bssn_fused<STAGE>, SMEM_FUSED, attr_done); e != cudaSuccess) return e;
+  const bool mon = STAGE == 1 && a.mon_partials != nullptr;
+  const void* fn = (const void*)bssn_fused<STAGE, false>;
+  if constexpr (STAGE == 1)
+    if (mon) fn = (const void*)bssn_fused<1, true>;
+  static std::atomic<uint64_t> attr_done[2];
+  if (cudaError_t e = smem_optin(fn, SMEM_FUSED, attr_done[mon ? 1 : 0]); e != cudaSuccess) return e;
 #ifdef CHEMORA_DEBUG_FUSED
   fprintf(stderr, "launch_fused<%d> optin\n", STAGE);
 #endif
@@ -483,7 +507,12 @@ cudaError_t launch_fused(const StageLaunch& a, const BssnK& K, double* dst, cuda
 #ifdef CHEMORA_DEBUG_FUSED
   fprintf(stderr, "launch_fused<%d> grid %d items %d chunk %d smem %d\n", STAGE, grid, nitems, chunk, SMEM_FUSED);
 #endif
-  bssn_fused<STAGE><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+  if constexpr (STAGE == 1) {
+    if (mon) bssn_fused<1, true><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+    else bssn_fused<1, false><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+  } else {
+    bssn_fused<STAGE, false><<<grid, FNT, SMEM_FUSED, st>>>(M, a, K, ntx, nty, chunk, nitems, dst);
+  }
   if (STAGE >= 1) {  // z ghost planes of the stage output (own wrap or the neighbours' slabs)
     double* out = const_cast<double*>(STAGE == 1 ? a.s.b : (STAGE == 2 ? a.s.c : (STAGE == 3 ? a.s.b : a.s.y)));
     if (cudaError_t e = push_z_planes(L, out, a.img[STAGE - 1], st); e != cudaSuccess) return e;
