@@ -10,7 +10,7 @@ for rep in 1 2; do
   for v in "$@"; do
     cp ab/lib$v.so $L
     echo -n "$v "
-    timeout 300 python bench.py $ARGS --no-cpu-baseline --e2e-steps 0 | \
+    timeout 120 python bench.py $ARGS --no-cpu-baseline --e2e-steps 0 | \
       python -c "import json,sys; print(json.loads(sys.stdin.read().strip().splitlines()[-1])['ms_per_step'])"
   done
 done
