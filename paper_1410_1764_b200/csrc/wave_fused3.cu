@@ -371,31 +371,53 @@ __global__ void __launch_bounds__(NT, 1)
           for (int f = 1; f <= 4; ++f) Qv[f] = qs[f * C1 + cc];
           yu = qs[5 * C1 + cc];
         }
+        // ghost images: only warps with a point near an x/y/z face take the image path (the
+        // tile rows of the interior -- most warps -- store the new values only)
+        const ImageSite isite = image_site(L, i, j, k);
+        const bool img = __any_sync(0xffffffffu, live && (isite.general || isite.single));
         if (live) {
           const int64_t c = cglob;
-          const ImageSite isite = image_site(L, i, j, k);
           if (!B) {
             double* outc = a.s.c;
             const FaceDst fd = a.img[1];
-            auto put = [&](int f, double v) {
-              outc[f * gfs + c] = v;
-              put_images(isite, outc + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
-            };
             auto putq = [&](int f, double v) { a.s.q[f * gfs + c] = v; };
-            wave_update<2>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            if (img) {
+              auto put = [&](int f, double v) {
+                outc[f * gfs + c] = v;
+                put_images(isite, outc + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
+              };
+              wave_update<2>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            } else {
+              auto put = [&](int f, double v) { outc[f * gfs + c] = v; };
+              wave_update<2>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            }
           } else {
             double* outy = a.s.b;  // the new state goes to the scratch set (swapped by the caller)
             const FaceDst fd = a.img[0];
+            const bool mon = a.mon_partials != nullptr;
             double esq = 0.0;  // rho^2 + v.v of the new state (fused energy monitor)
-            auto put = [&](int f, double v) {
-              outy[f * gfs + c] = v;
-              put_images(isite, outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
-              // branch-free non-finite check (NaN and +-Inf fail |v| <= DBL_MAX)
-              bad |= (fabs(v) <= 1.7976931348623157e308 ? 0u : 1u) << f;
-              if (f >= 1) esq += v * v;
-            };
+            double chk = 0.0;  // 0 * v: NaN once any new value is non-finite
             auto putq = [&](int, double) {};
-            wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            if (img) {
+              auto put = [&](int f, double v) {
+                outy[f * gfs + c] = v;
+                put_images(isite, outy + f * gfs, fd.lo + f * gfs, fd.hi + f * gfs, L, i, j, k, c, v);
+                chk = fma(v, 0.0, chk);
+                if (mon && f >= 1) esq += v * v;
+              };
+              wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            } else {
+              auto put = [&](int f, double v) {
+                outy[f * gfs + c] = v;
+                chk = fma(v, 0.0, chk);
+                if (mon && f >= 1) esq += v * v;
+              };
+              wave_update<4>(K, S, kk, Y, Qv, yu, qu, put, putq);
+            }
+            // (rare) which GFs: re-read the values this thread just stored
+            if (chk != 0.0)
+#pragma unroll
+              for (int f = 0; f < 5; ++f) bad |= (fabs(outy[f * gfs + c]) <= 1.7976931348623157e308 ? 0u : 1u) << f;
             eacc += 0.5 * esq;
           }
         }
