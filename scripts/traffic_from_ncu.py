@@ -1,0 +1,68 @@
+"""Per-launch DRAM traffic of the dominant kernels from ncu launch lists -> profiles/r2_traffic.json.
+
+The bench line's ``roofline.traffic`` is read from that file (bench.committed_traffic):
+dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over the launches of the
+timed-like steps (the last ``--steps`` full steps in the list).
+
+usage: python scripts/traffic_from_ncu.py WAVE_CSV BSSN_CSV [SOURCE_NOTE]
+"""
+import csv
+import json
+import os
+import re
+import sys
+from collections import defaultdict
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def launches(path):
+    """[(id, kernel name, {metric: value})] in launch order."""
+    rows = [l for l in open(path) if l.startswith('"')]
+    rd = csv.DictReader(rows)
+    by = {}
+    for r in rd:
+        k = int(r["ID"])
+        e = by.setdefault(k, [r["Kernel Name"], {}])
+        v = r["Metric Value"].replace(",", "")
+        e[1][r["Metric Name"]] = float(v) if v not in ("", "n/a") else 0.0
+    return [(k, by[k][0], by[k][1]) for k in sorted(by)]
+
+
+def dram(m):
+    return m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+
+
+def wave(path):
+    acc = defaultdict(list)
+    for _, name, m in launches(path):
+        mm = re.search(r"wave_fused3<(\d)>", name)
+        if mm:
+            acc["wave_fused3<%s>" % "AB"[int(mm.group(1))]].append(dram(m))
+    return {k: sum(v[-2:]) / len(v[-2:]) for k, v in acc.items()}
+
+
+def bssn(path):
+    acc = defaultdict(list)
+    for _, name, m in launches(path):
+        mm = re.search(r"bssn_fused<(?:\(int\))?(\d)", name)
+        if mm:
+            acc["bssn_stage%s" % mm.group(1)].append(dram(m))
+    return {k: v[-1] for k, v in sorted(acc.items())}
+
+
+if __name__ == "__main__":
+    note = sys.argv[3] if len(sys.argv) > 3 else ""
+    w, b = wave(sys.argv[1]), bssn(sys.argv[2])
+    out = {
+        "_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (cold-cache, serialised "
+                 "launch lists of the bench commands). " + note,
+        "wave512": w,
+        "bssn192": b,
+        "wave512_step_bytes": sum(w.values()),
+        "bssn192_step_bytes": sum(b.values()),
+    }
+    p = os.path.join(HERE, "..", "profiles", "r2_traffic.json")
+    with open(p, "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(json.dumps(out, indent=1))
