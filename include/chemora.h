@@ -232,7 +232,8 @@ int chemora_set_phase_barrier(chemora_grid_t grid, void (*fn)(void* user), void*
  * PAPER.md:642-644): when enabled, the kernel of every chemora_rk4_step(_multi) step that
  * writes the new state (the stage-4 kernel, or the stage-pair kernel B of the temporally
  * blocked path) also reduces E = h^3 sum eps of that state over the LOCAL slab
- * (deterministic per-CTA partials + a fixed-order sum) -- no extra HBM pass over the state.
+ * (deterministic partials per CTA or per work item + a fixed-order sum) -- no extra HBM pass
+ * over the state.
  * BSSN: the constraint monitors H, M^i, G^i (R16) of the state
  * entering every step, reduced by the step's stage-1 kernel (kernel design 4: from the
  * derivatives it computes anyway; other designs: the constraint kernel before stage 1).

@@ -169,7 +169,7 @@ WsPlan plan_ws(const Layout& L, int system, int nranks) {
   p.params = off;
   off += align256(sizeof(double) * kParams);
   p.flags = off;
-  off += align256(sizeof(unsigned long long) * 4);
+  off += align256(sizeof(unsigned long long) * 8);  // nan flag, 2 phase flags, -, 2 scheduler words
   // NEXT-3 fused energy monitor (wave): per-CTA partials of the stage-4 launch (any CTA
   // shape 32 x BY x BZ with BY * BZ = 8) and a ring of per-step energies
   p.mon_n = 0;
@@ -382,6 +382,7 @@ StageLaunch stage_args(chemora_grid_t g, double dt) {
   a.params = g->dparams;
   for (int i = 0; i < kParams; ++i) a.hparams[i] = g->params[i];
   a.nan_flag = g->nan_flag;
+  a.sched = g->nan_flag + 4;
   a.step = g->step;
   a.k_begin = 0;
   a.k_end = (int)g->L.nz;
@@ -544,7 +545,7 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
   // slower under the power cap (profiles/r1_wave_summary.md); autotune may pick it (-1)
   g->band = 0;
-  unsigned long long init[3] = {~0ull, 0ull, 0ull};
+  unsigned long long init[8] = {~0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
   cudaError_t e = cudaMemcpy(g->dparams, g->params, sizeof(g->params), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(fl, init, sizeof(init), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {

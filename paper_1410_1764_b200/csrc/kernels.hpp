@@ -33,6 +33,9 @@ struct StageLaunch {
   const double* params;  // device copy of BSSN gauge params (10)
   double hparams[10];    // host copy (folded into kernel arguments)
   unsigned long long* nan_flag;
+  // dynamic work scheduler of the persistent wave pair kernels: [0] next item, [1] CTAs done;
+  // zero between launches (the last CTA of a launch resets both)
+  unsigned long long* sched;
   uint64_t step;         // global step index (for the non-finite report)
   int k_begin, k_end;    // local z-plane range [k_begin, k_end)
   int variant;           // kernel variant (0 = default fast, 1 = simple reference kernel)

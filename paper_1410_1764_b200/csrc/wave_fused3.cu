@@ -54,6 +54,13 @@ constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermed
 // the z ring holds planes p-5 .. p (6 slots), the v1/v2 ring planes p-3 .. p (4 slots).
 constexpr int LAG = 3;
 constexpr int RI_Z = 4, RI_P = 4;   // planes p-3 .. p
+// items (tile x z-chunk) are handed out dynamically (an atomic counter, in order), so the
+// items in flight at any time are neighbours in (x, y): their shared halo rows are read by
+// both while still in L2.  (With a static round-robin assignment the persistent CTAs drift
+// apart by tens of planes over a launch and the halos are read from HBM twice.)  The
+// producer passes each item index to its consumers through a small shared queue, published
+// by the mbarrier of the item's first input plane.
+constexpr int IQ = 4;
 
 template <bool B> struct Geo {
   // input ring depths: resident windows are Z: planes p-3 .. p+2 (6), P: p-3 .. p (A) or p
@@ -72,7 +79,9 @@ template <bool B> struct Geo {
   static constexpr int OFF_IP = OFF_IZ + RI_Z * IZ_B;
   static constexpr int OFF_BAR = OFF_IP + RI_P * IP_B;
   static constexpr int NBAR = 2 * RZ + 2 * RP + 2 * RQ;
-  static constexpr int SMEM = OFF_BAR + NBAR * 8;
+  static constexpr int OFF_ITEMQ = OFF_BAR + NBAR * 8;
+  static constexpr int OFF_RED = OFF_ITEMQ + 4 * IQ + 8;  // energy partials, 2 x NCW doubles
+  static constexpr int SMEM = OFF_RED + 16 * NCW;
   static_assert(SMEM <= 232448, "shared memory");
 };
 
@@ -104,6 +113,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* pempty = pfull + G::RP;
   uint64_t* qfull = pempty + G::RP;
   uint64_t* qempty = qfull + G::RQ;
+  int* itemq = reinterpret_cast<int*>(smem + G::OFF_ITEMQ);
   const Layout& L = a.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -118,8 +128,19 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == NCW) {  // ------------------------------------------------------ producer
     if (lane != 0) return;
-    uint32_t nz = 0, np = 0, nq = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    uint32_t nz = 0, np = 0, nq = 0, nit = 0;
+    for (;;) {
+      const int item = (int)atomicAdd(a.sched, 1ull);
+      {  // the item index (or the end marker) travels with the item's first input slot
+        const uint32_t s = nz % G::RZ, n = nz / G::RZ;
+        if (n > 0) mbar_wait_suspend(zempty + s, (n - 1) & 1);
+        itemq[nit % IQ] = item;
+        ++nit;
+        if (item >= nitems) {
+          mbar_arrive(zfull + s);  // completes the slot's phase with no data: end of work
+          break;
+        }
+      }
       const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
       const int i0 = bx * TX, j0 = by * TY;
       const int kb = a.k_begin + ch * kchunk;
@@ -171,6 +192,11 @@ __global__ void __launch_bounds__(NT, 1)
       if (B)
         for (int k = kb + nk + 2 - LAG; k < kb + nk; ++k) loadQ(k);
     }
+    // the last CTA to finish fetching resets the scheduler for the next launch
+    if (atomicAdd(a.sched + 1, 1ull) == gridDim.x - 1) {
+      a.sched[0] = 0ull;
+      a.sched[1] = 0ull;
+    }
     return;
   }
 
@@ -220,15 +246,19 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr int PYR = PY_R / 8, PY1 = PY_1 / 8, PY2 = PY_2 / 8;
   const double C1W = D1W<W>::c(1), C2W = D1W<W>::c(2);
 
-  double eacc = 0.0;  // this thread's energy sum (B, monitor on), in a fixed point order
+  double eacc = 0.0;  // this thread's energy sum over the current item (B, monitor on)
   uint32_t bad = 0;   // B: bit f set once GF f produced a non-finite value (reported at the end)
-  uint32_t nz = 0, np = 0, nq = 0;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  uint32_t nz = 0, np = 0, nq = 0, nit = 0;
+  for (;;) {
+    const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
+    mbar_wait(zfull + z0 % G::RZ, (z0 / G::RZ) & 1);  // the item's first input plane, or the end
+    const int item = itemq[nit % IQ];
+    ++nit;
+    if (item >= nitems) break;
     const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
     const int i0 = bx * TX, j0 = by * TY;
     const int kb = a.k_begin + ch * kchunk;
     const int nk = min(kchunk, a.k_begin + nkall - kb);
-    const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
     for (int q = 0; q < 4; ++q) mbar_wait(zfull + (z0 + q) % G::RZ, ((z0 + q) / G::RZ) & 1);
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
@@ -461,25 +491,27 @@ __global__ void __launch_bounds__(NT, 1)
     }
     nz = z0 + nk + 8;
     np = p0 + nk + 4;
+    // NEXT-3 fused energy monitor (Fig. 1 "Energy"): one partial per item
+    // (tile x z-chunk), a fixed shuffle tree then warps in order, so the per-step energy does
+    // not depend on which CTA ran the item
+    if (B && a.mon_partials) {
+      double v = eacc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      double* red = reinterpret_cast<double*>(smem + G::OFF_RED) + (nit & 1) * NCW;  // double-buffered
+      if (lane == 0) red[warp] = v;
+      cbar();
+      if (tid == 0) {
+        double sum = 0.0;
+        for (int w = 0; w < NCW; ++w) sum += red[w];
+        a.mon_partials[item] = sum;
+      }
+      eacc = 0.0;
+    }
   }
   // the first non-finite GF of this thread (the flag keeps min(step * n_gf + gf) over threads)
   if (B && bad) check_finite(a.nan_flag, a.step * (unsigned long long)a.L.n_gf + (unsigned long long)(__ffs(bad) - 1),
                              __longlong_as_double(0x7ff8000000000000ll));
-  // NEXT-3 fused energy monitor (Fig. 1 "Energy"): one partial per CTA,
-  // fixed shuffle tree then warps in order, so the per-step energy is deterministic
-  if (B && a.mon_partials) {
-    __shared__ double red[NCW];
-    double v = eacc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp] = v;
-    cbar();
-    if (tid == 0) {
-      double sum = 0.0;
-      for (int w = 0; w < NCW; ++w) sum += red[w];
-      a.mon_partials[blockIdx.x] = sum;
-    }
-  }
 }
 
 bool enc(CUtensorMap* m, const double* set, const Layout& L, unsigned bx, unsigned by, unsigned bg) {
