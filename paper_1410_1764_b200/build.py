@@ -54,10 +54,11 @@ def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        cmd = ["nvcc", *ARCH, "-shared", "-o", OUT + ".tmp", *objs]
-        subprocess.check_call(cmd)
-        os.replace(OUT + ".tmp", OUT)
+    # always relink (a few seconds): an mtime test would keep a library copied in from
+    # elsewhere (e.g. an A/B build) whose timestamp is newer than the objects
+    cmd = ["nvcc", *ARCH, "-shared", "-o", OUT + ".tmp", *objs]
+    subprocess.check_call(cmd)
+    os.replace(OUT + ".tmp", OUT)
     return OUT
 
 

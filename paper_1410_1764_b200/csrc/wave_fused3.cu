@@ -67,7 +67,7 @@ template <bool B> struct Geo {
   // (B), Q: k (B); the rest is prefetch
   static constexpr int RZ = B ? 8 : 10;
   static constexpr int RP = B ? 3 : 8;
-  static constexpr int RQ = B ? 3 : 0;
+  static constexpr int RQ = B ? 3 : 1;  // (A: one unused slot pair keeps the ring arithmetic defined)
   static constexpr int PSLOT = P1_B + P2_B + (B ? PY_R + PY_1 + PY_2 + PY_3 : 0);
   static constexpr uint32_t PBYTES =
       (B1_X * B1_Y + B2_X * B2_Y + (B ? IR_X * IR_Y + I1_X * I1_Y + I2_X * I2_Y + I3_X * I3_Y : 0)) * 8;
