@@ -101,7 +101,9 @@ __device__ __forceinline__ double d1s_(const double* f, int c, int s) {
 
 __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"r"(32 * NCW) : "memory"); }
 
-template <bool B>
+// MON: kernel B with the fused energy monitor (its own instantiation: the default kernel
+// carries none of the monitor's work)
+template <bool B, bool MON>
 __global__ void __launch_bounds__(NT, 1)
     wave_fused3(const __grid_constant__ FMaps M, StageLaunch a, WaveK K, int kchunk, int ntx, int nty, int nitems) {
   using G = Geo<B>;
@@ -263,6 +265,11 @@ __global__ void __launch_bounds__(NT, 1)
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
     int64_t cglob = L.idx(i, j, kb);  // global offset of this thread's point at plane k
+    // ghost images (see image_site): the x/y part is fixed for the item; only warps with a
+    // point near an x or y face -- or any warp on a plane near a z face -- store images
+    const bool nxf = i < L.g || i >= L.nx - L.g, nyf = j < L.g || j >= L.ny - L.g;
+    const int64_t ioff = nxf ? (int64_t)(i < L.g ? L.nx : -L.nx) : (int64_t)(j < L.g ? L.ny : -L.ny) * L.px;
+    const bool img_xy = __any_sync(0xffffffffu, live && (nxf || nyf));
     int zsl[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) zsl[q] = (int)((z0 + G::RZ + q - 1) % G::RZ);
@@ -403,8 +410,9 @@ __global__ void __launch_bounds__(NT, 1)
         }
         // ghost images: only warps with a point near an x/y/z face take the image path (the
         // tile rows of the interior -- most warps -- store the new values only)
-        const ImageSite isite = image_site(L, i, j, k);
-        const bool img = __any_sync(0xffffffffu, live && (isite.general || isite.single));
+        const bool kface = k < L.g || k >= L.nz - L.g;
+        const ImageSite isite{kface || (nxf && nyf), nxf || nyf, ioff};
+        const bool img = img_xy || kface;
         if (live) {
           const int64_t c = cglob;
           if (!B) {
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(NT, 1)
           } else {
             double* outy = a.s.b;  // the new state goes to the scratch set (swapped by the caller)
             const FaceDst fd = a.img[0];
-            const bool mon = a.mon_partials != nullptr;
+            constexpr bool mon = MON;
             double esq = 0.0;  // rho^2 + v.v of the new state (fused energy monitor)
             double chk = 0.0;  // 0 * v: NaN once any new value is non-finite
             auto putq = [&](int, double) {};
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(NT, 1)
             if (chk != 0.0)
 #pragma unroll
               for (int f = 0; f < 5; ++f) bad |= (fabs(outy[f * gfs + c]) <= 1.7976931348623157e308 ? 0u : 1u) << f;
-            eacc += 0.5 * esq;
+            if (MON) eacc += 0.5 * esq;
           }
         }
         cglob += L.plane;
@@ -494,7 +502,7 @@ __global__ void __launch_bounds__(NT, 1)
     // NEXT-3 fused energy monitor (Fig. 1 "Energy"): one partial per item
     // (tile x z-chunk), a fixed shuffle tree then warps in order, so the per-step energy does
     // not depend on which CTA ran the item
-    if (B && a.mon_partials) {
+    if (B && MON) {
       double v = eacc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -526,7 +534,7 @@ WaveK make_k(const StageLaunch& a) {
   return K;
 }
 
-template <bool B>
+template <bool B, bool MON>
 cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
   using G = Geo<B>;
   const int nk = a.k_end - a.k_begin;
@@ -541,7 +549,7 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
             enc(&M.q5, a.s.q, L, TX, TY, 5) && enc(&M.yu, a.s.y, L, TX, TY, 1);
   if (!ok) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> attr_done{0};
-  if (cudaError_t e = smem_optin((const void*)wave_fused3<B>, G::SMEM, attr_done); e != cudaSuccess) return e;
+  if (cudaError_t e = smem_optin((const void*)wave_fused3<B, MON>, G::SMEM, attr_done); e != cudaSuccess) return e;
   const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
   // z planes per item (128: measured best of 32..512 at 512^3): longer chunks recompute
@@ -557,7 +565,7 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
   const int nitems = ntx * nty * nchunks;
   const int grid = nitems < nsm ? nitems : nsm;
   const WaveK K = make_k(a);
-  wave_fused3<B><<<grid, NT, G::SMEM, st>>>(M, a, K, chunk, ntx, nty, nitems);
+  wave_fused3<B, MON><<<grid, NT, G::SMEM, st>>>(M, a, K, chunk, ntx, nty, nitems);
   return cudaGetLastError();
 }
 
@@ -565,7 +573,8 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
 
 cudaError_t wave_fused3_pair(const StageLaunch& a, int pair, cudaStream_t st) {
   if (a.fd_order != 4) return cudaErrorInvalidValue;
-  return pair == 0 ? launch<false>(a, st) : launch<true>(a, st);
+  return pair == 0 ? launch<false, false>(a, st)
+                   : (a.mon_partials ? launch<true, true>(a, st) : launch<true, false>(a, st));
 }
 
 }  // namespace chemora
