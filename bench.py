@@ -69,14 +69,28 @@ def fp64_peaks():
     return derived, meas
 
 
-def committed_traffic(config: str, kernel: str):
-    """ncu dram__bytes_read+write per launch of `kernel` from the committed --set full capture
-    (profiles/r2_traffic.json), or None."""
+def committed_traffic(config: str, kernel, key=None):
+    """ncu dram__bytes_read+write per launch of `kernel` from the committed launch lists
+    (profiles/r2_traffic.json, scripts/traffic_from_ncu.py), or a top-level `key`; None if absent."""
     p = os.path.join(HERE, "profiles", "r2_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
-        return json.load(fh).get(config, {}).get(kernel)
+        d = json.load(fh)
+    return d.get(key) if key else d.get(config, {}).get(kernel)
+
+
+def oracle_opcount(what: str):
+    """Flops per point from the op-counting instantiation of the oracle (committed output of
+    scripts/oracle_opcount.cpp), or None."""
+    p = os.path.join(HERE, "profiles", "r2_oracle_opcount.jsonl")
+    if not os.path.exists(p):
+        return None
+    for line in open(p):
+        d = json.loads(line)
+        if d.get("what") == what:
+            return d["flops"]
+    return None
 
 
 class ClockSampler:
@@ -413,6 +427,18 @@ def main():
                         "alg_flops_note": "SURVEY.md §8(d): ~22.7 k flops per point-update (FMA = 2)",
                         "launch_ms_avg": avg[dom], "launch_share_of_step": share,
                         "hbm_frac_at_2400_bytes": BSSN_BYTES * pts_local / mean_step_s / 1e9 / measured_peaks()[0]}
+            # SURVEY 8(d)'s op-counting instantiation of the oracle (scripts/oracle_opcount.cpp,
+            # profiles/r2_oracle_opcount.jsonl): the oracle's full-3x3 formulation, an upper
+            # bound of the method's flops; and the kernels' executed fp64 instructions (ncu)
+            oc = oracle_opcount("BSSN RK4 step per point")
+            if oc:
+                roofline["oracle_count_flops_per_point_step"] = oc
+                roofline["frac_at_oracle_count"] = oc / 4 * pts_local / (avg[dom] * 1e-3) / 1e12 / derived
+            fi = committed_traffic(config, None, "bssn192_fp64_thread_instr_per_point_step")
+            if fi and meas and meas.get("sustained"):
+                roofline["kernel_fp64_instr_per_point_step"] = fi
+                roofline["fp64_instr_rate_frac_of_measured_dfma"] = \
+                    fi * pts_local / mean_step_s / (meas["sustained"] * 1e12 / 2)
             if meas and meas.get("sustained"):
                 roofline["peak_measured_sustained"] = meas["sustained"]
                 roofline["peak_measured_burst"] = meas["burst"]

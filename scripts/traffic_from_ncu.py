@@ -43,17 +43,18 @@ def wave(path):
 
 
 def bssn(path):
-    acc = defaultdict(list)
+    acc, fp64 = defaultdict(list), defaultdict(list)
     for _, name, m in launches(path):
         mm = re.search(r"bssn_fused<(?:\(int\))?(\d)", name)
         if mm:
             acc["bssn_stage%s" % mm.group(1)].append(dram(m))
-    return {k: v[-1] for k, v in sorted(acc.items())}
+            fp64[mm.group(1)].append(m.get("sm__inst_executed_pipe_fp64.sum", 0.0))
+    return {k: v[-1] for k, v in sorted(acc.items())}, sum(v[-1] for v in fp64.values())
 
 
 if __name__ == "__main__":
     note = sys.argv[3] if len(sys.argv) > 3 else ""
-    w, b = wave(sys.argv[1]), bssn(sys.argv[2])
+    w, (b, fp64_warp_instr) = wave(sys.argv[1]), bssn(sys.argv[2])
     out = {
         "_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (cold-cache, serialised "
                  "launch lists of the bench commands). " + note,
@@ -61,6 +62,8 @@ if __name__ == "__main__":
         "bssn192": b,
         "wave512_step_bytes": sum(w.values()),
         "bssn192_step_bytes": sum(b.values()),
+        # executed fp64 thread instructions (DFMA = 1) per point per RK4 step of the BSSN kernels
+        "bssn192_fp64_thread_instr_per_point_step": fp64_warp_instr * 32 / 192 ** 3,
     }
     p = os.path.join(HERE, "..", "profiles", "r2_traffic.json")
     with open(p, "w") as fh:
