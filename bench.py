@@ -82,7 +82,7 @@ def committed_traffic(config: str, kernel, key=None):
 
 def oracle_opcount(what: str):
     """Flops per point from the op-counting instantiation of the oracle (committed output of
-    scripts/oracle_opcount.cpp), or None."""
+    tests/oracle_opcount.cpp), or None."""
     p = os.path.join(HERE, "profiles", "r2_oracle_opcount.jsonl")
     if not os.path.exists(p):
         return None
@@ -427,7 +427,7 @@ def main():
                         "alg_flops_note": "SURVEY.md §8(d): ~22.7 k flops per point-update (FMA = 2)",
                         "launch_ms_avg": avg[dom], "launch_share_of_step": share,
                         "hbm_frac_at_2400_bytes": BSSN_BYTES * pts_local / mean_step_s / 1e9 / measured_peaks()[0]}
-            # SURVEY 8(d)'s op-counting instantiation of the oracle (scripts/oracle_opcount.cpp,
+            # SURVEY 8(d)'s op-counting instantiation of the oracle (tests/oracle_opcount.cpp,
             # profiles/r2_oracle_opcount.jsonl): the oracle's full-3x3 formulation, an upper
             # bound of the method's flops; and the kernels' executed fp64 instructions (ncu)
             oc = oracle_opcount("BSSN RK4 step per point")

@@ -2,14 +2,15 @@
 // flops come from an op-counting instantiation of the oracle RHS: templated on a counting
 // scalar type that counts +, -, x, /, fma and exp").
 //
-// MEASUREMENT INFRASTRUCTURE (like bench.py's cpu_baseline leg): the oracle source is
+// TEST INFRASTRUCTURE (run by tests/test_oracle_opcount.py, which also checks that the
+// committed profiles/r2_oracle_opcount.jsonl equals a fresh run): the oracle source is
 // compiled unchanged, with its scalar type `double` replaced by the counting type Cnt, so
 // every floating-point operation of the oracle's formulation is counted exactly; nothing
 // of the CUDA path is involved.  The oracle writes its tensors as full 3x3 index loops
 // (symmetric entries computed twice), so these counts are an upper bound of the method's
 // flops; SURVEY.md's 22.7k per BSSN RK4 step is the symmetric-packed estimate.
 //
-// build + run:  g++ -O1 -std=c++17 -I. scripts/oracle_opcount.cpp -o /tmp/opcount && /tmp/opcount
+// build + run:  g++ -O1 -std=c++17 -I. tests/oracle_opcount.cpp -o /tmp/opcount && /tmp/opcount
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
