@@ -286,7 +286,7 @@ def main():
                     help="skip the BSSN 192^3 secondary line and the configs[0] report")
     # e2e steps: enough that the pipeline fill (first upload) and drain (last download) are
     # amortised -- per step the two PCIe directions then overlap (scripts/pcie_probe.py)
-    ap.add_argument("--e2e-steps", type=int, default=12)
+    ap.add_argument("--e2e-steps", type=int, default=24)
     ap.add_argument("--variant", type=int, default=None, help="stage-kernel variant (testing)")
     ap.add_argument("--fd-order", type=int, default=4, choices=[2, 4, 6, 8],
                     help="wave: accuracy order of the centered stencils (NEXT-1, PAPER.md:512-514)")
