@@ -415,6 +415,12 @@ def main():
                 d = WAVE_PAIR_DESIGN_BYTES[dom]
                 roofline["design_bytes_per_point_per_launch"] = d
                 roofline["frac_at_design_bytes"] = d * pts_local / (avg[dom] * 1e-3) / 1e9 / peak
+                roofline["frac_note"] = ("frac can exceed 1: SURVEY 8(d)'s 432 B/pt counts one HBM pass per RK "
+                                         "substep, the temporally blocked stage pairs move fewer bytes (design "
+                                         "256 B/pt); frac_at_design_bytes is the kernel against its own floor, "
+                                         "dram_frac_measured its ncu-measured traffic over its live duration")
+                if roofline["traffic"] and config == "wave512":
+                    roofline["dram_frac_measured"] = roofline["traffic"] / (avg[dom] * 1e-3) / 1e9 / peak
         else:
             derived, meas = fp64_peaks()
             flops = BSSN_FLOPS / 4 * pts_local

@@ -36,7 +36,7 @@ def dram(m):
 def wave(path):
     acc = defaultdict(list)
     for _, name, m in launches(path):
-        mm = re.search(r"wave_fused3<(\d)>", name)
+        mm = re.search(r"wave_fused3<(?:\(bool\))?(\d)", name)
         if mm:
             acc["wave_fused3<%s>" % "AB"[int(mm.group(1))]].append(dram(m))
     return {k: sum(v[-2:]) / len(v[-2:]) for k, v in acc.items()}
