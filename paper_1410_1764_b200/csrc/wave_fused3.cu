@@ -50,10 +50,14 @@ constexpr int PY_R = r128(IR_X * IR_Y * 8), PY_1 = r128(I1_X * I1_Y * 8), PY_2 =
 constexpr int IZ_B = r128(IR_X * IR_Y * 8);  // intermediate rho ring slot (v3 lives in registers)
 constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermediate p ring slot
 // The second stage runs 3 planes behind the first (k = p - 3), so within one iteration the
-// two stages touch disjoint intermediate slots and a single CTA barrier per plane suffices:
-// the z ring holds planes p-5 .. p (6 slots), the v1/v2 ring planes p-3 .. p (4 slots).
+// two stages touch disjoint intermediate slots.  The intermediate rings hold 5 planes
+// (p-4 .. p): iteration t writes slot t mod 5, which the second stage last read in iteration
+// t-2, and reads the slot written in t-3.  So the warps need not meet at a CTA barrier every
+// plane: each arrives on a per-iteration mbarrier when done and, before writing, waits only
+// until every warp has finished iteration t-2 (the warps may drift one plane apart).
 constexpr int LAG = 3;
-constexpr int RI_Z = 4, RI_P = 4;   // planes p-3 .. p
+constexpr int RI_Z = 5, RI_P = 5;
+constexpr int ND = 4;               // per-iteration "done" mbarriers, used round robin
 // items (tile x z-chunk) are handed out dynamically (an atomic counter, in order), so the
 // items in flight at any time are neighbours in (x, y): their shared halo rows are read by
 // both while still in L2.  (With a static round-robin assignment the persistent CTAs drift
@@ -78,7 +82,7 @@ template <bool B> struct Geo {
   static constexpr int OFF_IZ = OFF_Q + RQ * QSLOT;
   static constexpr int OFF_IP = OFF_IZ + RI_Z * IZ_B;
   static constexpr int OFF_BAR = OFF_IP + RI_P * IP_B;
-  static constexpr int NBAR = 2 * RZ + 2 * RP + 2 * RQ;
+  static constexpr int NBAR = 2 * RZ + 2 * RP + 2 * RQ + ND;
   static constexpr int OFF_ITEMQ = OFF_BAR + NBAR * 8;
   static constexpr int OFF_RED = OFF_ITEMQ + 4 * IQ + 8;  // energy partials, 2 x NCW doubles
   static constexpr int SMEM = OFF_RED + 16 * NCW;
@@ -115,6 +119,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* pempty = pfull + G::RP;
   uint64_t* qfull = pempty + G::RP;
   uint64_t* qempty = qfull + G::RQ;
+  uint64_t* done = qempty + G::RQ;
   int* itemq = reinterpret_cast<int*>(smem + G::OFF_ITEMQ);
   const Layout& L = a.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int s = 0; s < G::RZ; ++s) { mbar_init(zfull + s, 1); mbar_init(zempty + s, NCW); }
     for (int s = 0; s < G::RP; ++s) { mbar_init(pfull + s, 1); mbar_init(pempty + s, NCW); }
     for (int s = 0; s < G::RQ; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, NCW); }
+    for (int s = 0; s < ND; ++s) mbar_init(done + s, NCW);
     fence_mbar_init();
   }
   __syncthreads();
@@ -251,6 +257,8 @@ __global__ void __launch_bounds__(NT, 1)
   double eacc = 0.0;  // this thread's energy sum over the current item (B, monitor on)
   uint32_t bad = 0;   // B: bit f set once GF f produced a non-finite value (reported at the end)
   uint32_t nz = 0, np = 0, nq = 0, nit = 0;
+  uint32_t t = 0;  // iterations of this CTA's warps over all items
+  int wslot = 0;   // t mod RI_Z: the intermediate slot written in iteration t
   for (;;) {
     const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
     mbar_wait(zfull + z0 % G::RZ, (z0 / G::RZ) & 1);  // the item's first input plane, or the end
@@ -291,11 +299,13 @@ __global__ void __launch_bounds__(NT, 1)
       const bool second = k >= kb;              // output plane k
 #pragma unroll
       for (int q = 0; q < 3; ++q) izs[q] = izs[q + 1];
-      izs[3] = jj % RI_Z;
+      izs[3] = wslot;
 #pragma unroll
       for (int q = 0; q < 3; ++q) ips[q] = ips[q + 1];
-      ips[3] = jj % RI_P;
-      cbar();  // the previous plane's intermediate values are complete and its reads done
+      ips[3] = wslot;
+      // every warp has finished iteration t-2: the slot written now was last read there, and
+      // the slot read now (written in t-3) is complete
+      if (t >= 2) mbar_wait(done + (t - 2) % ND, ((t - 2) / ND) & 1);
       double IRown = 0.0, I3own = 0.0;
       if (first) {
         mbar_wait(zfull + zsl[5], zph);
@@ -478,7 +488,10 @@ __global__ void __launch_bounds__(NT, 1)
           mbar_arrive(pempty + psl);                      // planes kb-2, kb-1: no second stage
         }
         if (jj >= 1) mbar_arrive(zempty + zsl[0]);        // input plane p - 3
+        mbar_arrive(done + t % ND);                       // this warp is done with iteration t
       }
+      ++t;
+      wslot = wslot + 1 == RI_Z ? 0 : wslot + 1;
       if (B && second) ++nq;
       // ---- advance the rings
 #pragma unroll
