@@ -56,7 +56,7 @@ struct Cfg {
   static constexpr int RP = RZ * ZSLOT + 3 * PSLOT + (2 * RZ + 6) * 8 <= 227 * 1024 ? 3 : 2;
   static constexpr uint32_t ZBYTES = (RX * RY + C) * 8;
   static constexpr uint32_t PBYTES = (RX * TY + TX * RY + (PW<STAGE>::NY + PW<STAGE>::NQ + PW<STAGE>::NU) * C) * 8;
-  static constexpr int SMEM = RZ * ZSLOT + RP * PSLOT + (2 * RZ + 2 * RP) * 8;
+  static constexpr int SMEM = RZ * ZSLOT + RP * PSLOT + (2 * RZ + 2 * RP) * 8 + 16;  // + item queue
   static constexpr int THREADS = 32 * (NCW + 1);
 };
 
@@ -91,6 +91,12 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
   uint64_t* zempty = zfull + Cf::RZ;
   uint64_t* pfull = zempty + Cf::RZ;
   uint64_t* pempty = pfull + Cf::RP;
+  // items are handed out in order by an atomic counter (as in wave_fused3.cu: the items in
+  // flight stay (x,y) neighbours, so shared halo rows are re-read from L2); the producer
+  // passes each index to the consumers through this queue, published by the mbarrier of the
+  // item's first input plane
+  int* itemq = reinterpret_cast<int*>(pempty + Cf::RP);
+  constexpr int IQ = 4;
   const Layout& L = a.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -108,8 +114,19 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
     if (P::NY) prefetch_tmap(&M.y4);
     if (P::NU) prefetch_tmap(&M.yu);
     if (P::NQ) prefetch_tmap(&M.q);
-    uint32_t nz = 0, np = 0;  // running load counters (ring position and phase)
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    uint32_t nz = 0, np = 0, nit = 0;  // running load counters (ring position and phase)
+    for (;;) {
+      const int item = (int)atomicAdd(a.sched, 1ull);
+      {  // the item index (or the end marker) travels with the item's first input slot
+        const uint32_t s = nz % Cf::RZ, n = nz / Cf::RZ;
+        if (n > 0) mbar_wait(zempty + s, (n - 1) & 1);
+        itemq[nit % IQ] = item;
+        ++nit;
+        if (item >= nitems) {
+          mbar_arrive(zfull + s);  // completes the slot's phase with no data: end of work
+          break;
+        }
+      }
       const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
       const int i0 = bx * Cf::TX, j0 = by * Cf::TY;
       const int kb = a.k_begin + ch * kchunk;
@@ -145,6 +162,11 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
         loadP(kb + t);
       }
     }
+    // the last CTA to finish fetching resets the scheduler for the next launch
+    if (atomicAdd(a.sched + 1, 1ull) == gridDim.x - 1) {
+      a.sched[0] = 0ull;
+      a.sched[1] = 0ull;
+    }
     return;
   }
 
@@ -156,8 +178,12 @@ __global__ void __launch_bounds__(Cfg<STAGE, W>::THREADS, 1)
   const int ty = warp, tx = lane;
   const int cr = (ty + Cf::H) * Cf::RX + (tx + Cf::H);  // rho box index
   const int cv = ty * Cf::TX + tx;              // centre box index
-  uint32_t nz = 0, np = 0;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  uint32_t nz = 0, np = 0, nit = 0;
+  for (;;) {
+    mbar_wait(zfull + nz % Cf::RZ, (nz / Cf::RZ) & 1);  // the item's first input plane, or the end
+    const int item = itemq[nit % IQ];
+    ++nit;
+    if (item >= nitems) break;
     const int bx = item % ntx, by = (item / ntx) % nty, ch = item / (ntx * nty);
     const int i = bx * Cf::TX + tx, j = by * Cf::TY + ty;
     const int kb = a.k_begin + ch * kchunk;
