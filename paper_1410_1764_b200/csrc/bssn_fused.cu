@@ -37,12 +37,10 @@ constexpr int FR = 3;                                  // halo (upwind radius)
 // (an odd fp64 start column faults the bulk-tensor copy) and spans 24 doubles
 constexpr int FRX = 4;
 constexpr int FSX = FX + 2 * FRX, FSY = FY + 2 * FR, FPL = FSX * FSY;   // 24 x 14
-#ifndef FUSED_NGRP
-#define FUSED_NGRP 2
-#endif
-// equation groups per point: 2 = {G2, G13} at 255 registers (8 warps/SM); 3 = {G2, G1, G3} at
-// 168 registers (12 warps/SM)
-constexpr int NGRP = FUSED_NGRP;
+// two threads per point: the curvature group G2 and the kinematic + shift group G13 at 255
+// registers, 8 warps per SM (three groups at 168 registers, 12 warps, spilled and measured
+// slower: profiles/r2_bssn_summary.md)
+constexpr int NGRP = 2;
 constexpr int FNT = NGRP * FPT;                        // (point, group) threads
 constexpr int NWARP = FNT / 32;
 constexpr int NMIX = 11;                               // GFs with mixed second derivatives
@@ -58,24 +56,14 @@ constexpr int NMON = 14;                               // constraint monitor: [s
 constexpr int FEED_PL = FPT;                            // doubles per GF (1 KB)
 constexpr int FEED_STRIDE = NV * FEED_PL * 8;           // bytes per buffer (25.6 KB)
 constexpr int SMEM_FUSED = 2 * TILE_STRIDE + 2 * FEED_STRIDE + 8 * (GZX_N + GZY_N + GYX_N) + 64 + 8 * NWARP * NMON;
-// TMEM window feed split over the groups: [0, 9) [9, 17) [17, 25) (3 groups) or [0, 13) [13, 25)
-// -- the 11 GFs with mixed derivatives stay with one group each (phi, gt: 0; alpha, beta: last)
-constexpr int FEED_B1 = NGRP == 3 ? 9 : 13, FEED_B2 = NGRP == 3 ? 17 : 25;
-constexpr int FEEDN = NGRP == 3 ? 9 : 13;             // max GFs fed by one thread
+// TMEM window feed split over the groups: [0, 13) [13, 25) -- the 11 GFs with mixed
+// derivatives stay with one group each (phi, gt: G2's threads; alpha, beta: G13's)
+constexpr int FEED_B1 = 13;
+constexpr int FEEDN = 13;                              // max GFs fed by one thread
 constexpr int NFRAME = 2 * 2 * FY + 2 * 2 * FX;        // 2-point x- and y-frames of the tile: 96
 constexpr int NFI = (NMIX * NFRAME + FNT - 1) / FNT;   // frame items per thread (5)
 
 // ---- TMEM (tcgen05) helpers: each thread reads / writes its own lane
-#ifdef FUSED_NO_TMEM
-__device__ __forceinline__ void tm_ld16(uint32_t, uint32_t (&r)[16]) {
-  for (int q = 0; q < 16; ++q) r[q] = 0u;
-}
-__device__ __forceinline__ void tm_st16(uint32_t, const uint32_t (&)[16]) {}
-__device__ __forceinline__ void tm_wait_ld() {}
-__device__ __forceinline__ void tm_wait_st() {}
-__device__ __forceinline__ void tm_fence_before() {}
-__device__ __forceinline__ void tm_fence_after() {}
-#else
 __device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -95,7 +83,6 @@ __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sy
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-#endif
 __device__ __forceinline__ double dbl(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
 __device__ __forceinline__ void cta_sync_tm() {
   tm_fence_before();
@@ -211,14 +198,10 @@ __global__ void __launch_bounds__(FNT, 1)
   const double* in = stage_input<STAGE>(a);
   const int ntiles = ntx * nty;
 
-#ifndef FUSED_NO_TMEM
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-#else
-  if (tid == 0) *tmem_slot = 0;
-#endif
   if (tid == 0) {
     for (int q = 0; q < 2; ++q) { mbar_init(&mbar[q], 1); mbar_init(&fbar[q], 1); }
     fence_mbar_init();
@@ -237,16 +220,11 @@ __global__ void __launch_bounds__(FNT, 1)
     ke = min(kb + chunk, a.k_end);
   };
   auto issue_tile = [&](int buf, int i0, int j0, int k) {
-#ifdef FUSED_NO_TMA
-    mbar_arrive(&mbar[buf]);
-    (void)i0; (void)j0; (void)k;
-#else
     mbar_arrive_expect_tx(&mbar[buf], (uint32_t)TILE_BYTES);
 #pragma unroll 1
     for (int q = 0; q < NV; ++q)  // one box per GF (a GF plane per 128-byte aligned slot)
       tma_load_4d(tiles + (size_t)buf * (TILE_STRIDE / 8) + q * FPLS, &M.in, &mbar[buf], kXOff + i0 - FRX,
                   L.g + j0 - FR, L.g + k, q);
-#endif
   };
   auto issue_feed = [&](int buf, int i0, int j0, int k) {  // tile interior of plane k, all GFs
     mbar_arrive_expect_tx(&fbar[buf], (uint32_t)FEED_STRIDE);
@@ -275,8 +253,7 @@ __global__ void __launch_bounds__(FNT, 1)
     // the ghost zone: live neighbours read their D1_z through the mixed-derivative helpers
     const int ic = min(i, xhi), jc = min(j, yhi);
     const double* col = in + (int64_t)jc * L.px + ic;                   // own column, plane 0, GF 0
-    const int g_lo = grp == 0 ? 0 : (grp == 1 ? FEED_B1 : FEED_B2);
-    const int g_hi = grp == 0 ? FEED_B1 : (grp == 1 ? FEED_B2 : NV);
+    const int g_lo = grp == 0 ? 0 : FEED_B1, g_hi = grp == 0 ? FEED_B1 : NV;  // this thread's feed GFs
     // frame item geometry of this thread, recomputed per plane (cheap integer work; keeping
     // it live across the algebra would cost registers)
     auto frame_item = [&](int m, int& dst) -> int64_t {
@@ -337,7 +314,7 @@ __global__ void __launch_bounds__(FNT, 1)
         const double* pre = (STAGE == 4 ? a.s.q : a.s.y) + L.idx(i, j, k);
 #pragma unroll
         for (int v = 0; v < NV; ++v)
-          if (grp == 0 ? in_group(2, v) : (NGRP == 2 ? in_group(13, v) : (grp == 1 ? in_group(1, v) : in_group(3, v))))
+          if (grp == 0 ? in_group(2, v) : in_group(13, v))
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pre + v * gfs));
       }
       // ... the own column two planes ahead of the feed pulled into L2 (its first touch is
@@ -403,20 +380,14 @@ __global__ void __launch_bounds__(FNT, 1)
       if (grp == 0) {
         bssn_point<2>(P, K, r);
         if (live) bssn_update_src<STAGE, 2, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
-      } else if (NGRP == 2) {
+      } else {
         bssn_point<13>(P, K, r);
         if (live) bssn_update_src<STAGE, 13, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
-      } else if (grp == 1) {
-        bssn_point<1>(P, K, r);
-        if (live) bssn_update_src<STAGE, 1, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
-      } else {
-        bssn_point<3>(P, K, r);
-        if (live) bssn_update_src<STAGE, 3, TileIn, true>(a, K, r, tin, c, i, j, k, rhs_dst);
       }
       if constexpr (monitor) {
         // NEXT-3 fused constraint monitor: H, M^i, G^i of the state entering
         // this step (stage 1's input, already on chip), reduced per warp in a fixed order
-        if (monitor && (grp == 0 || grp == NGRP - 1)) {  // H by the G2 warps, M and G by the last group
+        {  // H by the G2 warps, M and G by the G13 warps
           double cv[7];
           if (grp == 0) bssn_constraint_point<1>(P, K, cv);
           else bssn_constraint_point<2>(P, K, cv);
@@ -440,9 +411,7 @@ __global__ void __launch_bounds__(FNT, 1)
       cta_sync_tm();
     }
   }
-#ifndef FUSED_NO_TMEM
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
-#endif
   if (monitor && tid < NMON) {  // warps in order: deterministic per-CTA partials
     double v = macc[tid];
     for (int w = 1; w < NWARP; ++w) v = (tid & 1) ? fmax(v, macc[w * NMON + tid]) : v + macc[w * NMON + tid];
