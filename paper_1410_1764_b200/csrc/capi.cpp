@@ -101,6 +101,15 @@ int radius_of(const chemora_grid_desc& d) {
   return 3;  // BSSN: lopsided upwind stencils reach 3 points
 }
 
+// storage ghost width: the temporally blocked wave kernels (wave_fused3.cu, orders 2 and 4)
+// read their inputs with a halo of two stacked radius-W stencils, so those grids keep at least
+// 2W ghost layers in HBM; the API's ghost width (desc.ghost) is unchanged.
+int storage_ghost(const chemora_grid_desc& d) {
+  const int order = d.fd_order == 0 ? 4 : d.fd_order;
+  if (d.system == CHEMORA_SYS_WAVE && (order == 2 || order == 4)) return std::max(d.ghost, order);
+  return d.ghost;
+}
+
 int validate(const chemora_grid_desc* d) {
   if (!d) return fail(CHEMORA_E_INVALID, "desc is NULL");
   const int nf = n_gf_of(d->system);
@@ -132,11 +141,10 @@ int validate(const chemora_grid_desc* d) {
   if (d->extent[2] / d->nranks < 2 * d->ghost)
     return fail(CHEMORA_E_SHAPE, "local slab must have >= 2*ghost planes");
   {
-    // the storage ghost width (>= 4 for 4th-order wave grids, see layout_of) must also fit
-    const int gs = (d->system == CHEMORA_SYS_WAVE && (d->fd_order == 0 || d->fd_order == 4) && d->ghost < 4)
-                       ? 4 : d->ghost;
+    // the storage ghost width (see layout_of) must also fit
+    const int gs = storage_ghost(*d);
     if (d->extent[0] < 2 * gs || d->extent[1] < 2 * gs || d->extent[2] / d->nranks < 2 * gs)
-      return fail(CHEMORA_E_SHAPE, "4th-order wave grids need >= 8 points per axis (and per slab)");
+      return fail(CHEMORA_E_SHAPE, "wave grids of order 2W need >= 4W points per axis (and per slab)");
   }
   if (d->n_params < 0 || (d->n_params > 0 && !d->params) || d->n_params > kParams)
     return fail(CHEMORA_E_INVALID, "bad params");
@@ -194,12 +202,7 @@ WsPlan plan_ws(const Layout& L, int system, int nranks) {
 }
 
 Layout layout_of(const chemora_grid_desc& d) {
-  // storage ghost width: the temporally blocked wave kernels (wave_fused3.cu) read their
-  // inputs with a halo of two stacked 4th-order stencils, so 4th-order wave grids keep at
-  // least 4 ghost layers in HBM; the API's ghost width (desc.ghost) is unchanged.
-  int gs = d.ghost;
-  if (d.system == CHEMORA_SYS_WAVE && (d.fd_order == 0 || d.fd_order == 4) && gs < 4) gs = 4;
-  return make_layout(d.extent[0], d.extent[1], d.extent[2] / d.nranks, gs, d.n_gf);
+  return make_layout(d.extent[0], d.extent[1], d.extent[2] / d.nranks, storage_ghost(d), d.n_gf);
 }
 
 SetPtrs sets_at(char* ws, const Layout& L) {
@@ -404,7 +407,8 @@ constexpr int kVariantFused3 = 8;
 bool is_fused_variant(int v) { return v == kVariantFused3; }
 bool use_fused(chemora_grid_t g) {
   const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
-  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order == 4 && g->L.g >= 4;
+  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && (order == 2 || order == 4) &&
+         g->L.g >= order;
 }
 cudaError_t fused_pair(int variant, const StageLaunch& a, int pair, cudaStream_t st) {
   (void)variant;
@@ -530,17 +534,17 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->ipc = false;
   g->cur = 0;
   // default tiling: the temporally blocked stage pairs with register-queue z stencils for
-  // 4th-order wave grids (variant 8, fastest measured, profiles/r1_wave_design_study.md);
-  // orders 6/8: the persistent TMA z-march when its 32x16 tiles fill the SMs (variant 4:
-  // 14.2 vs 15.6-18.1 ms/step at 512^3, profiles/r1_fd_orders.jsonl), else one thread per
-  // point (also for order 2, where it is fastest); BSSN: the fused per-stage kernel with the
-  // derivatives on chip (variant 4: as fast as the HBM-table fission, variant 3, at 192^3 with
-  // a fifth of its DRAM traffic, profiles/r2_bssn_summary.md)
+  // wave grids of order 2 and 4 (variant 8, fastest measured: order 4 profiles/r1_wave_design_study.md,
+  // order 2 7.2 vs 10.5 ms/step at 512^3, profiles/r2_fd_orders.jsonl); orders 6/8: the
+  // persistent TMA z-march when its 32x16 tiles fill the SMs (variant 4: 12.3 vs 15.6-18.1
+  // ms/step at 512^3), else one thread per point; BSSN: the fused per-stage kernel with the
+  // derivatives on chip (variant 4: faster than the HBM-table fission, variant 3, at 192^3
+  // with a fifth of its DRAM traffic, profiles/r2_bssn_summary.md)
   {
     const int order = desc->fd_order == 0 ? 4 : desc->fd_order;
     const int64_t tiles16 = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     g->variant = desc->system == CHEMORA_SYS_BSSN ? 4 /* fused, SMEM tiles + TMEM z-windows */
-               : order == 4 ? kVariantFused3 : (order >= 6 && tiles16 >= 148) ? 4 : 0;
+               : (order == 2 || order == 4) ? kVariantFused3 : (order >= 6 && tiles16 >= 148) ? 4 : 0;
   }
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
   // slower under the power cap (profiles/r1_wave_summary.md); autotune may pick it (-1)
@@ -842,7 +846,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     if (tiles >= 148) cands.push_back({4, 0});
-    if (order == 4 && g->L.g >= 4) {
+    if ((order == 2 || order == 4) && g->L.g >= order) {
       cands.push_back({kVariantFused3, 0});
     } else {
       cands.push_back({0, -1});

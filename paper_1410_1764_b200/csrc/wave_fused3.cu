@@ -24,64 +24,76 @@ namespace {
 using namespace wave;
 
 constexpr int TX = 32, TY = 8, NCW = 8, NT = 32 * (NCW + 1);
-constexpr int W = 2;   // 4th-order stencils (fd_order 4 only)
-constexpr int H = 4;   // input halo: two stacked radius-2 stencils
 constexpr int r128(int b) { return (b + 127) / 128 * 128; }
-
-// input box geometries (x extent, y extent, x origin offset, y origin offset)
-constexpr int BR_X = TX + 2 * H, BR_Y = TY + 2 * H;      // rho   (40 x 16), origin (-4,-4)
-constexpr int B3_X = TX + 2 * W, B3_Y = TY + 2 * W;      // v3    (36 x 12), origin (-2,-2)
-constexpr int B1_X = TX + 2 * H, B1_Y = TY + 2 * W;      // v1    (40 x 12), origin (-4,-2)
-constexpr int B2_X = TX + 2 * W, B2_Y = TY + 2 * H;      // v2    (36 x 16), origin (-2,-4)
-// intermediate-state geometries
-constexpr int IR_X = TX + 2 * W, IR_Y = TY + 2 * W;      // rho   (36 x 12), origin (-2,-2)
-constexpr int I1_X = TX + 2 * W, I1_Y = TY;              // v1    (36 x 8),  origin (-2, 0)
-constexpr int I2_X = TX, I2_Y = TY + 2 * W;              // v2    (32 x 12), origin ( 0,-2)
-constexpr int I3_X = TX, I3_Y = TY;                      // v3    (32 x 8)
-// pointwise boxes of kernel B (y on the intermediate geometries, Q and y.u centres)
-constexpr int C1 = TX * TY;
-
-constexpr int ZR_B = r128(BR_X * BR_Y * 8), Z3_B = r128(B3_X * B3_Y * 8);
-constexpr int ZSLOT = ZR_B + Z3_B;
-constexpr uint32_t ZBYTES = (BR_X * BR_Y + B3_X * B3_Y) * 8;
-constexpr int P1_B = r128(B1_X * B1_Y * 8), P2_B = r128(B2_X * B2_Y * 8);
-constexpr int PY_R = r128(IR_X * IR_Y * 8), PY_1 = r128(I1_X * I1_Y * 8), PY_2 = r128(I2_X * I2_Y * 8),
-              PY_3 = r128(I3_X * I3_Y * 8);
-constexpr int IZ_B = r128(IR_X * IR_Y * 8);  // intermediate rho ring slot (v3 lives in registers)
-constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermediate p ring slot
-// The second stage runs 3 planes behind the first (k = p - 3), so within one iteration the
-// two stages touch disjoint intermediate slots.  The intermediate rings hold 5 planes
-// (p-4 .. p): iteration t writes slot t mod 5, which the second stage last read in iteration
-// t-2, and reads the slot written in t-3.  So the warps need not meet at a CTA barrier every
-// plane: each arrives on a per-iteration mbarrier when done and, before writing, waits only
-// until every warp has finished iteration t-2 (the warps may drift one plane apart).
-constexpr int LAG = 3;
-constexpr int RI_Z = 5, RI_P = 5;
+constexpr int C1 = TX * TY;         // points per tile plane
+constexpr int IQ = 4;               // item queue (see the producer)
 constexpr int ND = 4;               // per-iteration "done" mbarriers, used round robin
+
+// Geometry of the stage pair for stencil radius W (FD order 2W; W = 2: the 4th-order default).
+// Boxes are [y][x] planes around the 32x8 tile; a box's x origin is rounded down to an even
+// offset (a TMA box whose fp64 rows start at an odd column faults), so for odd W the x-extended
+// boxes carry one unused column at each side.
+template <int W> struct PG {
+  static constexpr int H = 2 * W;                 // input halo: two stacked radius-W stencils
+  static constexpr int WX = (W + 1) / 2 * 2;      // x halo of the W-extended boxes, even
+  // input boxes (x extent, y extent; x origin, y origin relative to the tile)
+  static constexpr int BR_X = TX + 2 * H, BR_Y = TY + 2 * H, BR_OX = -H, BR_OY = -H;     // rho
+  static constexpr int B3_X = TX + 2 * WX, B3_Y = TY + 2 * W, B3_OX = -WX, B3_OY = -W;  // v3
+  static constexpr int B1_X = TX + 2 * H, B1_Y = TY + 2 * W, B1_OX = -H, B1_OY = -W;     // v1
+  static constexpr int B2_X = TX + 2 * WX, B2_Y = TY + 2 * H, B2_OX = -WX, B2_OY = -H;  // v2
+  // intermediate-state geometries (the same x rounding: kernel B loads y on them by TMA)
+  static constexpr int IR_X = TX + 2 * WX, IR_Y = TY + 2 * W, IR_OX = -WX, IR_OY = -W;  // rho
+  static constexpr int I1_X = TX + 2 * WX, I1_Y = TY, I1_OX = -WX, I1_OY = 0;           // v1
+  static constexpr int I2_X = TX, I2_Y = TY + 2 * W, I2_OX = 0, I2_OY = -W;             // v2
+  static constexpr int I3_X = TX, I3_Y = TY;                                            // v3
+  // halo elements computed by the first stage (logical, radius W): the IR ring, the I1 side
+  // columns, the I2 top / bottom rows
+  static constexpr int NHR = (TX + 2 * W) * (TY + 2 * W) - TX * TY, NH1 = 2 * W * TY, NH2 = 2 * W * TX;
+  static constexpr int NH2T = (NH2 + 63) / 64;    // I2 halo elements per thread (threads 0..63)
+  static constexpr int ZR_B = r128(BR_X * BR_Y * 8), Z3_B = r128(B3_X * B3_Y * 8);
+  static constexpr int ZSLOT = ZR_B + Z3_B;
+  static constexpr uint32_t ZBYTES = (BR_X * BR_Y + B3_X * B3_Y) * 8;
+  static constexpr int P1_B = r128(B1_X * B1_Y * 8), P2_B = r128(B2_X * B2_Y * 8);
+  static constexpr int PY_R = r128(IR_X * IR_Y * 8), PY_1 = r128(I1_X * I1_Y * 8), PY_2 = r128(I2_X * I2_Y * 8),
+                       PY_3 = r128(I3_X * I3_Y * 8);
+  static constexpr int IZ_B = r128(IR_X * IR_Y * 8);  // intermediate rho ring slot (v3 lives in registers)
+  static constexpr int IP_B = r128(I1_X * I1_Y * 8) + r128(I2_X * I2_Y * 8);  // intermediate p ring slot
+  // The second stage runs LAG = W+1 planes behind the first (k = p - LAG), so within one
+  // iteration the two stages touch disjoint intermediate slots.  The intermediate rings hold
+  // LAG+2 planes: iteration t writes slot t mod (LAG+2), which the second stage last read in
+  // iteration t-2, and reads the slot written in t-LAG.  So the warps need not meet at a CTA
+  // barrier every plane: each arrives on a per-iteration mbarrier when done and, before
+  // writing, waits only until every warp has finished iteration t-2 (the warps may drift one
+  // plane apart).
+  static constexpr int LAG = W + 1;
+  static constexpr int RI = LAG + 2;
+  static_assert(NHR <= 32 * NCW - 64 && NH1 <= 32 * NCW && W >= 1, "halo map");
+};
 // items (tile x z-chunk) are handed out dynamically (an atomic counter, in order), so the
 // items in flight at any time are neighbours in (x, y): their shared halo rows are read by
 // both while still in L2.  (With a static round-robin assignment the persistent CTAs drift
 // apart by tens of planes over a launch and the halos are read from HBM twice.)  The
 // producer passes each item index to its consumers through a small shared queue, published
 // by the mbarrier of the item's first input plane.
-constexpr int IQ = 4;
 
-template <bool B> struct Geo {
-  // input ring depths: resident windows are Z: planes p-3 .. p+2 (6), P: p-3 .. p (A) or p
+template <int W, bool B> struct Geo {
+  using Q = PG<W>;
+  // input ring depths: resident windows are Z: planes p-LAG .. p+W, P: p-LAG .. p (A) or p
   // (B), Q: k (B); the rest is prefetch
   static constexpr int RZ = B ? 8 : 10;
   static constexpr int RP = B ? 3 : 8;
   static constexpr int RQ = B ? 3 : 1;  // (A: one unused slot pair keeps the ring arithmetic defined)
-  static constexpr int PSLOT = P1_B + P2_B + (B ? PY_R + PY_1 + PY_2 + PY_3 : 0);
+  static constexpr int PSLOT = Q::P1_B + Q::P2_B + (B ? Q::PY_R + Q::PY_1 + Q::PY_2 + Q::PY_3 : 0);
   static constexpr uint32_t PBYTES =
-      (B1_X * B1_Y + B2_X * B2_Y + (B ? IR_X * IR_Y + I1_X * I1_Y + I2_X * I2_Y + I3_X * I3_Y : 0)) * 8;
+      (Q::B1_X * Q::B1_Y + Q::B2_X * Q::B2_Y +
+       (B ? Q::IR_X * Q::IR_Y + Q::I1_X * Q::I1_Y + Q::I2_X * Q::I2_Y + Q::I3_X * Q::I3_Y : 0)) * 8;
   static constexpr int QSLOT = B ? r128(6 * C1 * 8) : 0;  // Q (u, rho, v1..3) + y.u
   static constexpr uint32_t QBYTES = B ? 6 * C1 * 8 : 0;
-  static constexpr int OFF_P = RZ * ZSLOT;
+  static constexpr int OFF_P = RZ * Q::ZSLOT;
   static constexpr int OFF_Q = OFF_P + RP * PSLOT;
   static constexpr int OFF_IZ = OFF_Q + RQ * QSLOT;
-  static constexpr int OFF_IP = OFF_IZ + RI_Z * IZ_B;
-  static constexpr int OFF_BAR = OFF_IP + RI_P * IP_B;
+  static constexpr int OFF_IP = OFF_IZ + Q::RI * Q::IZ_B;
+  static constexpr int OFF_BAR = OFF_IP + Q::RI * Q::IP_B;
   static constexpr int NBAR = 2 * RZ + 2 * RP + 2 * RQ + ND;
   static constexpr int OFF_ITEMQ = OFF_BAR + NBAR * 8;
   static constexpr int OFF_RED = OFF_ITEMQ + 4 * IQ + 8;  // energy partials, 2 x NCW doubles
@@ -96,6 +108,7 @@ struct FMaps {
 };
 
 // shared-memory centered D1 (no 1/h), same operation order as wave::d1
+template <int W>
 __device__ __forceinline__ double d1s_(const double* f, int c, int s) {
   double acc = 0.0;
 #pragma unroll
@@ -107,10 +120,12 @@ __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"r"(32
 
 // MON: kernel B with the fused energy monitor (its own instantiation: the default kernel
 // carries none of the monitor's work)
-template <bool B, bool MON>
+template <int W, bool B, bool MON>
 __global__ void __launch_bounds__(NT, 1)
     wave_fused3(const __grid_constant__ FMaps M, StageLaunch a, WaveK K, int kchunk, int ntx, int nty, int nitems) {
-  using G = Geo<B>;
+  using G = Geo<W, B>;
+  using Q = PG<W>;
+  constexpr int H = Q::H, WX = Q::WX, LAG = Q::LAG;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* zfull = bars;
@@ -157,10 +172,10 @@ __global__ void __launch_bounds__(NT, 1)
       auto loadZ = [&](int plane) {
         const uint32_t s = nz % G::RZ, n = nz / G::RZ;
         if (n > 0) mbar_wait_suspend(zempty + s, (n - 1) & 1);
-        unsigned char* d = smem + s * ZSLOT;
-        mbar_arrive_expect_tx(zfull + s, ZBYTES);
-        tma_load_4d(d, &M.rho, zfull + s, xo - H, yo - H, g + plane, GRHO);
-        tma_load_4d(d + ZR_B, &M.v3, zfull + s, xo - W, yo - W, g + plane, GV3);
+        unsigned char* d = smem + s * Q::ZSLOT;
+        mbar_arrive_expect_tx(zfull + s, Q::ZBYTES);
+        tma_load_4d(d, &M.rho, zfull + s, xo + Q::BR_OX, yo + Q::BR_OY, g + plane, GRHO);
+        tma_load_4d(d + Q::ZR_B, &M.v3, zfull + s, xo + Q::B3_OX, yo + Q::B3_OY, g + plane, GV3);
         ++nz;
       };
       auto loadP = [&](int plane) {
@@ -169,14 +184,14 @@ __global__ void __launch_bounds__(NT, 1)
         unsigned char* d = smem + G::OFF_P + s * G::PSLOT;
         uint64_t* bar = pfull + s;
         mbar_arrive_expect_tx(bar, G::PBYTES);
-        tma_load_4d(d, &M.v1, bar, xo - H, yo - W, g + plane, GV1);
-        tma_load_4d(d + P1_B, &M.v2, bar, xo - W, yo - H, g + plane, GV2);
+        tma_load_4d(d, &M.v1, bar, xo + Q::B1_OX, yo + Q::B1_OY, g + plane, GV1);
+        tma_load_4d(d + Q::P1_B, &M.v2, bar, xo + Q::B2_OX, yo + Q::B2_OY, g + plane, GV2);
         if (B) {
-          unsigned char* e = d + P1_B + P2_B;
-          tma_load_4d(e, &M.yr, bar, xo - W, yo - W, g + plane, GRHO);
-          tma_load_4d(e + PY_R, &M.y1, bar, xo - W, yo, g + plane, GV1);
-          tma_load_4d(e + PY_R + PY_1, &M.y2, bar, xo, yo - W, g + plane, GV2);
-          tma_load_4d(e + PY_R + PY_1 + PY_2, &M.y3, bar, xo, yo, g + plane, GV3);
+          unsigned char* e = d + Q::P1_B + Q::P2_B;
+          tma_load_4d(e, &M.yr, bar, xo + Q::IR_OX, yo + Q::IR_OY, g + plane, GRHO);
+          tma_load_4d(e + Q::PY_R, &M.y1, bar, xo + Q::I1_OX, yo + Q::I1_OY, g + plane, GV1);
+          tma_load_4d(e + Q::PY_R + Q::PY_1, &M.y2, bar, xo + Q::I2_OX, yo + Q::I2_OY, g + plane, GV2);
+          tma_load_4d(e + Q::PY_R + Q::PY_1 + Q::PY_2, &M.y3, bar, xo, yo, g + plane, GV3);
         }
         ++np;
       };
@@ -189,16 +204,16 @@ __global__ void __launch_bounds__(NT, 1)
         tma_load_4d(d + 5 * C1 * 8, &M.yu, qfull + s, xo, yo, g + plane, GU);
         ++nq;
       };
-      // intermediate planes p = kb-2 .. kb+nk+1 need input planes p-2 .. p+2
-      for (int pl = kb - 4; pl < kb; ++pl) loadZ(pl);
-      for (int j = 0; j < nk + 4; ++j) {
-        const int p = kb - 2 + j;
-        loadZ(p + 2);
+      // intermediate planes p = kb-W .. kb+nk+W-1 need input planes p-W .. p+W
+      for (int pl = kb - 2 * W; pl < kb; ++pl) loadZ(pl);
+      for (int j = 0; j < nk + 2 * W; ++j) {
+        const int p = kb - W + j;
+        loadZ(p + W);
         loadP(p);
         if (B && p - LAG >= kb) loadQ(p - LAG);
       }
       if (B)
-        for (int k = kb + nk + 2 - LAG; k < kb + nk; ++k) loadQ(k);
+        for (int k = kb + nk + W - LAG; k < kb + nk; ++k) loadQ(k);
     }
     // the last CTA to finish fetching resets the scheduler for the next launch
     if (atomicAdd(a.sched + 1, 1ull) == gridDim.x - 1) {
@@ -213,54 +228,60 @@ __global__ void __launch_bounds__(NT, 1)
   const int64_t gfs = L.gfs;
   constexpr int NTC = 32 * NCW;
   const int ti = lane, tj = warp;  // this thread's output point of the tile
-  // the own point in the input boxes (origins: rho (-4,-4), v1 (-4,-2), v2 (-2,-4), v3 (-2,-2))
-  const int o_r = (tj + 4) * BR_X + ti + 4, o_1 = (tj + 2) * B1_X + ti + 4;
-  const int o_2 = (tj + 4) * B2_X + ti + 2, o_3 = (tj + 2) * B3_X + ti + 2;
-  // ... and in the intermediate geometries (IR (-2,-2), I1 (-2,0), I2 (0,-2))
-  const int e_R = (tj + 2) * IR_X + ti + 2, e_1 = tj * I1_X + ti + 2, e_2 = (tj + 2) * I2_X + ti;
+  // offset of logical point (x, y) (relative to the tile) in a box of width sx, origin (ox, oy)
+  auto at = [](int x, int y, int sx, int ox, int oy) { return (y - oy) * sx + (x - ox); };
+  // the own point in the input boxes and in the intermediate geometries
+  const int o_r = at(ti, tj, Q::BR_X, Q::BR_OX, Q::BR_OY), o_1 = at(ti, tj, Q::B1_X, Q::B1_OX, Q::B1_OY);
+  const int o_2 = at(ti, tj, Q::B2_X, Q::B2_OX, Q::B2_OY), o_3 = at(ti, tj, Q::B3_X, Q::B3_OX, Q::B3_OY);
+  const int e_R = at(ti, tj, Q::IR_X, Q::IR_OX, Q::IR_OY), e_1 = at(ti, tj, Q::I1_X, Q::I1_OX, Q::I1_OY);
+  const int e_2 = at(ti, tj, Q::I2_X, Q::I2_OX, Q::I2_OY);
   const int cc = tj * TX + ti;
-  // halo elements: IR ring of the 36x12 plane minus the 32x8 interior (176, threads 64..239),
-  // I1 columns x in {0,1,34,35} (32, warp 0), I2 rows y in {0,1,10,11} (128, threads 0..63 x 2)
-  const bool hR = tid >= 64 && tid < 64 + (IR_X * IR_Y - TX * TY);
+  // halo elements (logical radius W): the IR ring (threads 64 ..), the I1 side columns
+  // (threads 0 ..), the I2 top / bottom rows (threads 0..63, NH2T each)
+  const bool hR = tid >= 64 && tid < 64 + Q::NHR;
   int hR_c1 = 0, hR_c2 = 0, hR_c3 = 0, hR_b = 0, hR_e = 0;
   {
+    constexpr int RX = TX + 2 * W;  // logical IR row length
     const int h = hR ? tid - 64 : 0;
     int x, y;
-    if (h < 2 * IR_X) { y = h / IR_X; x = h % IR_X; }
-    else if (h < 4 * IR_X) { y = IR_Y - 2 + (h - 2 * IR_X) / IR_X; x = (h - 2 * IR_X) % IR_X; }
-    else { const int q = h - 4 * IR_X; y = 2 + q / 4; x = (q % 4) < 2 ? q % 4 : IR_X - 4 + q % 4; }
-    hR_c1 = y * B1_X + x + 2; hR_c2 = (y + 2) * B2_X + x; hR_c3 = y * B3_X + x;
-    hR_b = (y + 2) * BR_X + x + 2; hR_e = y * IR_X + x;
+    if (h < W * RX) { y = -W + h / RX; x = -W + h % RX; }
+    else if (h < 2 * W * RX) { y = TY + (h - W * RX) / RX; x = -W + (h - W * RX) % RX; }
+    else { const int q = h - 2 * W * RX, c = q % (2 * W); y = q / (2 * W); x = c < W ? -W + c : TX + c - W; }
+    hR_c1 = at(x, y, Q::B1_X, Q::B1_OX, Q::B1_OY); hR_c2 = at(x, y, Q::B2_X, Q::B2_OX, Q::B2_OY);
+    hR_c3 = at(x, y, Q::B3_X, Q::B3_OX, Q::B3_OY); hR_b = at(x, y, Q::BR_X, Q::BR_OX, Q::BR_OY);
+    hR_e = at(x, y, Q::IR_X, Q::IR_OX, Q::IR_OY);
   }
-  const bool h1 = tid < 32;
+  const bool h1 = tid < Q::NH1;
   int h1_cr, h1_b, h1_e;
   {
-    const int y = tid / 4 % I1_Y, q = tid % 4, x = q < 2 ? q : I1_X - 4 + q;
-    h1_cr = (y + 4) * BR_X + x + 2; h1_b = (y + 2) * B1_X + x + 2; h1_e = y * I1_X + x;
+    const int y = tid / (2 * W) % TY, c = tid % (2 * W), x = c < W ? -W + c : TX + c - W;
+    h1_cr = at(x, y, Q::BR_X, Q::BR_OX, Q::BR_OY); h1_b = at(x, y, Q::B1_X, Q::B1_OX, Q::B1_OY);
+    h1_e = at(x, y, Q::I1_X, Q::I1_OX, Q::I1_OY);
   }
   const bool h2 = tid < 64;
-  int h2_cr[2], h2_b[2], h2_e[2];
+  int h2_cr[Q::NH2T], h2_b[Q::NH2T], h2_e[Q::NH2T];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int h = (tid % 64) + 64 * u, r = h / I2_X, x = h % I2_X, y = r < 2 ? r : I2_Y - 4 + r;
-    h2_cr[u] = (y + 2) * BR_X + x + 4; h2_b[u] = (y + 2) * B2_X + x + 2; h2_e[u] = y * I2_X + x;
+  for (int u = 0; u < Q::NH2T; ++u) {
+    const int h = (tid % 64) + 64 * u, r = h / TX % (2 * W), x = h % TX, y = r < W ? -W + r : TY + r - W;
+    h2_cr[u] = at(x, y, Q::BR_X, Q::BR_OX, Q::BR_OY); h2_b[u] = at(x, y, Q::B2_X, Q::B2_OX, Q::B2_OY);
+    h2_e[u] = at(x, y, Q::I2_X, Q::I2_OX, Q::I2_OY);
   }
-  static_assert(IR_X * IR_Y - TX * TY == 176 && IR_X * IR_Y - TX * TY <= NTC - 64, "halo map");
+  static_assert(Q::NH2 == 64 * Q::NH2T, "I2 halo map");
   const double cdt = B ? K.dt : K.dt2;
   double* const sm = reinterpret_cast<double*>(smem);
-  constexpr int ZSD = ZSLOT / 8, ZR_D = ZR_B / 8, PSD = G::PSLOT / 8, P1D = P1_B / 8, P2D = P2_B / 8;
-  constexpr int IZD = IZ_B / 8, IPD = IP_B / 8, I1_D = r128(I1_X * I1_Y * 8) / 8;
+  constexpr int ZSD = Q::ZSLOT / 8, ZR_D = Q::ZR_B / 8, PSD = G::PSLOT / 8, P1D = Q::P1_B / 8, P2D = Q::P2_B / 8;
+  constexpr int IZD = Q::IZ_B / 8, IPD = Q::IP_B / 8, I1_D = r128(Q::I1_X * Q::I1_Y * 8) / 8;
   constexpr int OFF_PD = G::OFF_P / 8, OFF_QD = G::OFF_Q / 8, OFF_IZD = G::OFF_IZ / 8, OFF_IPD = G::OFF_IP / 8;
-  constexpr int PYR = PY_R / 8, PY1 = PY_1 / 8, PY2 = PY_2 / 8;
-  const double C1W = D1W<W>::c(1), C2W = D1W<W>::c(2);
+  constexpr int PYR = Q::PY_R / 8, PY1 = Q::PY_1 / 8, PY2 = Q::PY_2 / 8;
+  constexpr int NZW = 2 * W + 1;  // z window of a stencil: planes -W .. +W
 
   double eacc = 0.0;  // this thread's energy sum over the current item (B, monitor on)
   uint32_t bad = 0;   // B: bit f set once GF f produced a non-finite value (reported at the end)
   uint32_t nz = 0, np = 0, nq = 0, nit = 0;
   uint32_t t = 0;  // iterations of this CTA's warps over all items
-  int wslot = 0;   // t mod RI_Z: the intermediate slot written in iteration t
+  int wslot = 0;   // t mod RI: the intermediate slot written in iteration t
   for (;;) {
-    const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-4, of P plane kb-2
+    const uint32_t z0 = nz, p0 = np;  // ring index of input plane kb-2W, of P plane kb-W
     mbar_wait(zfull + z0 % G::RZ, (z0 / G::RZ) & 1);  // the item's first input plane, or the end
     const int item = itemq[nit % IQ];
     ++nit;
@@ -269,7 +290,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int i0 = bx * TX, j0 = by * TY;
     const int kb = a.k_begin + ch * kchunk;
     const int nk = min(kchunk, a.k_begin + nkall - kb);
-    for (int q = 0; q < 4; ++q) mbar_wait(zfull + (z0 + q) % G::RZ, ((z0 + q) / G::RZ) & 1);
+    for (int q = 0; q < 2 * W; ++q) mbar_wait(zfull + (z0 + q) % G::RZ, ((z0 + q) / G::RZ) & 1);
     const int i = i0 + ti, j = j0 + tj;
     const bool live = i < L.nx && j < L.ny;
     int64_t cglob = L.idx(i, j, kb);  // global offset of this thread's point at plane k
@@ -278,98 +299,98 @@ __global__ void __launch_bounds__(NT, 1)
     const bool nxf = i < L.g || i >= L.nx - L.g, nyf = j < L.g || j >= L.ny - L.g;
     const int64_t ioff = nxf ? (int64_t)(i < L.g ? L.nx : -L.nx) : (int64_t)(j < L.g ? L.ny : -L.ny) * L.px;
     const bool img_xy = __any_sync(0xffffffffu, live && (nxf || nyf));
-    int zsl[6];
+    int zsl[NZW + 1];                           // input slots of planes p-LAG .. p+W
 #pragma unroll
-    for (int q = 0; q < 6; ++q) zsl[q] = (int)((z0 + G::RZ + q - 1) % G::RZ);
-    int zph = (int)(((z0 + 4) / G::RZ) & 1);    // phase of the input slot zsl[5]
+    for (int q = 0; q <= NZW; ++q) zsl[q] = (int)((z0 + G::RZ + q - 1) % G::RZ);
+    int zph = (int)(((z0 + 2 * W) / G::RZ) & 1);  // phase of the input slot zsl[NZW]
     int psl = (int)(p0 % G::RP);                // P slot of plane p
     int pph = (int)((p0 / G::RP) & 1);
-    int pslk = psl;                             // P slot of plane k = p - 3 (A, jj >= 3)
-    int izs[4] = {0, 0, 0, 0};                  // intermediate rho slots of planes p-3 .. p
-    int ips[4] = {0, 0, 0, 0};                  // intermediate v1/v2 slots of planes p-3 .. p
-    // register queues (see the file header); index 0 is the oldest plane
-    double qIR[5], qI3[5];
+    int pslk = psl;                             // P slot of plane k = p - LAG (A, jj >= LAG)
+    int izs[LAG + 1] = {};                      // intermediate rho slots of planes p-LAG .. p
+    int ips[LAG + 1] = {};                      // intermediate v1/v2 slots of planes p-LAG .. p
+    // register queues (see the file header): planes p-2W-1 .. p-1, index 0 the oldest
+    double qIR[NZW], qI3[NZW];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) { qIR[q] = 0.0; qI3[q] = 0.0; }
+    for (int q = 0; q < NZW; ++q) { qIR[q] = 0.0; qI3[q] = 0.0; }
 #pragma unroll 1
-    for (int jj = 0; jj < nk + 4 + 1; ++jj) {
-      const int p = kb - 2 + jj;
-      const bool first = jj < nk + 4;           // intermediate plane p is needed
+    for (int jj = 0; jj < nk + 2 * W + 1; ++jj) {
+      const int p = kb - W + jj;
+      const bool first = jj < nk + 2 * W;       // intermediate plane p is needed
       const int k = p - LAG;
       const bool second = k >= kb;              // output plane k
 #pragma unroll
-      for (int q = 0; q < 3; ++q) izs[q] = izs[q + 1];
-      izs[3] = wslot;
+      for (int q = 0; q < LAG; ++q) izs[q] = izs[q + 1];
+      izs[LAG] = wslot;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) ips[q] = ips[q + 1];
-      ips[3] = wslot;
+      for (int q = 0; q < LAG; ++q) ips[q] = ips[q + 1];
+      ips[LAG] = wslot;
       // every warp has finished iteration t-2: the slot written now was last read there, and
       // the slot read now (written in t-3) is complete
       if (t >= 2) mbar_wait(done + (t - 2) % ND, ((t - 2) / ND) & 1);
       double IRown = 0.0, I3own = 0.0;
       if (first) {
-        mbar_wait(zfull + zsl[5], zph);
+        mbar_wait(zfull + zsl[NZW], zph);
         mbar_wait(pfull + psl, pph);
-        const double* zR[5];
-        const double* z3[5];
+        const double* zR[NZW];  // input planes p-W .. p+W
+        const double* z3[NZW];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
+        for (int q = 0; q < NZW; ++q) {
           zR[q] = sm + zsl[q + 1] * ZSD;
           z3[q] = zR[q] + ZR_D;
         }
         const double* s1 = sm + OFF_PD + psl * PSD;
         const double* s2 = s1 + P1D;
         const double* sy = s2 + P2D;  // B only
-        double* IR = sm + OFF_IZD + izs[3] * IZD;
-        double* I1 = sm + OFF_IPD + ips[3] * IPD;
+        double* IR = sm + OFF_IZD + izs[LAG] * IZD;
+        double* I1 = sm + OFF_IPD + ips[LAG] * IPD;
         double* I2 = I1 + I1_D;
         // ---- intermediate state at plane p: Y2 = y + dt/2 k1(y) (A) or Y4 = y + dt k3(C) (B)
-        {  // rho at the own point; z neighbours of v3 from the queue (planes p-2 .. p+2)
-          const double dv1 = d1s_(s1, o_1, 1) * K.ih[0];
-          const double dv2 = d1s_(s2, o_2, B2_X) * K.ih[1];
+        {  // rho at the own point; z neighbours of v3 from the input planes p-W .. p+W
+          const double dv1 = d1s_<W>(s1, o_1, 1) * K.ih[0];
+          const double dv2 = d1s_<W>(s2, o_2, Q::B2_X) * K.ih[1];
           double dv3 = 0.0;
-          dv3 = fma(C2W, z3[4][o_3] - z3[0][o_3], dv3);
-          dv3 = fma(C1W, z3[3][o_3] - z3[1][o_3], dv3);
+#pragma unroll
+          for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[W + q][o_3] - z3[W - q][o_3], dv3);
           dv3 = dv3 * K.ih[2];
           const double kr = dv1 + dv2 + dv3;
-          const double base = B ? sy[e_R] : zR[2][o_r];
+          const double base = B ? sy[e_R] : zR[W][o_r];
           IRown = fma(cdt, kr, base);
           IR[e_R] = IRown;
         }
         if (hR) {  // rho at the halo element
-          const double dv1 = d1s_(s1, hR_c1, 1) * K.ih[0];
-          const double dv2 = d1s_(s2, hR_c2, B2_X) * K.ih[1];
+          const double dv1 = d1s_<W>(s1, hR_c1, 1) * K.ih[0];
+          const double dv2 = d1s_<W>(s2, hR_c2, Q::B2_X) * K.ih[1];
           double dv3 = 0.0;
-          dv3 = fma(C2W, z3[4][hR_c3] - z3[0][hR_c3], dv3);
-          dv3 = fma(C1W, z3[3][hR_c3] - z3[1][hR_c3], dv3);
+#pragma unroll
+          for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[W + q][hR_c3] - z3[W - q][hR_c3], dv3);
           dv3 = dv3 * K.ih[2];
           const double kr = dv1 + dv2 + dv3;
-          const double base = B ? sy[hR_e] : zR[2][hR_b];
+          const double base = B ? sy[hR_e] : zR[W][hR_b];
           IR[hR_e] = fma(cdt, kr, base);
         }
         {  // v1, v2 at the own point
-          const double k1v = d1s_(zR[2], o_r, 1) * K.ih[0];
+          const double k1v = d1s_<W>(zR[W], o_r, 1) * K.ih[0];
           I1[e_1] = fma(cdt, k1v, B ? sy[PYR + e_1] : s1[o_1]);
-          const double k2v = d1s_(zR[2], o_r, BR_X) * K.ih[1];
+          const double k2v = d1s_<W>(zR[W], o_r, Q::BR_X) * K.ih[1];
           I2[e_2] = fma(cdt, k2v, B ? sy[PYR + PY1 + e_2] : s2[o_2]);
         }
         if (h1) {
-          const double kr = d1s_(zR[2], h1_cr, 1) * K.ih[0];
+          const double kr = d1s_<W>(zR[W], h1_cr, 1) * K.ih[0];
           I1[h1_e] = fma(cdt, kr, B ? sy[PYR + h1_e] : s1[h1_b]);
         }
         if (h2) {
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const double kr = d1s_(zR[2], h2_cr[u], BR_X) * K.ih[1];
+          for (int u = 0; u < Q::NH2T; ++u) {
+            const double kr = d1s_<W>(zR[W], h2_cr[u], Q::BR_X) * K.ih[1];
             I2[h2_e[u]] = fma(cdt, kr, B ? sy[PYR + PY1 + h2_e[u]] : s2[h2_b[u]]);
           }
         }
         {  // v3 at the own point: z neighbours of rho from the queue; stays in registers
           double dzr = 0.0;
-          dzr = fma(C2W, zR[4][o_r] - zR[0][o_r], dzr);
-          dzr = fma(C1W, zR[3][o_r] - zR[1][o_r], dzr);
+#pragma unroll
+          for (int q = W; q >= 1; --q) dzr = fma(D1W<W>::c(q), zR[W + q][o_r] - zR[W - q][o_r], dzr);
           const double kr = dzr * K.ih[2];
-          const double base = B ? sy[PYR + PY1 + PY2 + cc] : z3[2][o_3];
+          const double base = B ? sy[PYR + PY1 + PY2 + cc] : z3[W][o_3];
           I3own = fma(cdt, kr, base);
         }
       }
@@ -380,20 +401,21 @@ __global__ void __launch_bounds__(NT, 1)
         const double* i1 = sm + OFF_IPD + ips[0] * IPD;
         const double* i2 = i1 + I1_D;
         double S[5], kk[5];
-        S[GRHO] = qIR[2];
+        S[GRHO] = qIR[W];
         S[GV1] = i1[e_1];
         S[GV2] = i2[e_2];
-        S[GV3] = qI3[2];
+        S[GV3] = qI3[W];
         double dzr = 0.0, dv3 = 0.0;
-        dzr = fma(C2W, qIR[4] - qIR[0], dzr);
-        dv3 = fma(C2W, qI3[4] - qI3[0], dv3);
-        dzr = fma(C1W, qIR[3] - qIR[1], dzr);
-        dv3 = fma(C1W, qI3[3] - qI3[1], dv3);
-        const double dxr = d1s_(iRk, e_R, 1) * K.ih[0];
-        const double dyr = d1s_(iRk, e_R, IR_X) * K.ih[1];
+#pragma unroll
+        for (int q = W; q >= 1; --q) {
+          dzr = fma(D1W<W>::c(q), qIR[W + q] - qIR[W - q], dzr);
+          dv3 = fma(D1W<W>::c(q), qI3[W + q] - qI3[W - q], dv3);
+        }
+        const double dxr = d1s_<W>(iRk, e_R, 1) * K.ih[0];
+        const double dyr = d1s_<W>(iRk, e_R, Q::IR_X) * K.ih[1];
         dzr = dzr * K.ih[2];
-        const double dv1 = d1s_(i1, e_1, 1) * K.ih[0];
-        const double dv2 = d1s_(i2, e_2, I2_X) * K.ih[1];
+        const double dv1 = d1s_<W>(i1, e_1, 1) * K.ih[0];
+        const double dv2 = d1s_<W>(i2, e_2, Q::I2_X) * K.ih[1];
         dv3 = dv3 * K.ih[2];
         kk[GRHO] = dv1 + dv2 + dv3;
         kk[GV1] = dxr;
@@ -473,9 +495,9 @@ __global__ void __launch_bounds__(NT, 1)
       }
       // intermediate queues: push the own values of plane p
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { qIR[q] = qIR[q + 1]; qI3[q] = qI3[q + 1]; }
-      qIR[4] = IRown;
-      qI3[4] = I3own;
+      for (int q = 0; q < NZW - 1; ++q) { qIR[q] = qIR[q + 1]; qI3[q] = qI3[q + 1]; }
+      qIR[NZW - 1] = IRown;
+      qI3[NZW - 1] = I3own;
       // ---- release what this warp has finished reading
       __syncwarp();
       if (lane == 0) {
@@ -484,34 +506,34 @@ __global__ void __launch_bounds__(NT, 1)
           if (first) mbar_arrive(pempty + psl);          // P plane p (first stage only)
         } else if (second) {
           mbar_arrive(pempty + pslk);                     // P plane k
-        } else if (jj < 2) {
-          mbar_arrive(pempty + psl);                      // planes kb-2, kb-1: no second stage
+        } else if (jj < W) {
+          mbar_arrive(pempty + psl);                      // planes kb-W .. kb-1: no second stage
         }
-        if (jj >= 1) mbar_arrive(zempty + zsl[0]);        // input plane p - 3
+        if (jj >= 1) mbar_arrive(zempty + zsl[0]);        // input plane p - LAG
         mbar_arrive(done + t % ND);                       // this warp is done with iteration t
       }
       ++t;
-      wslot = wslot + 1 == RI_Z ? 0 : wslot + 1;
+      wslot = wslot + 1 == Q::RI ? 0 : wslot + 1;
       if (B && second) ++nq;
       // ---- advance the rings
 #pragma unroll
-      for (int q = 0; q < 5; ++q) zsl[q] = zsl[q + 1];
-      zsl[5] = zsl[4] + 1 == G::RZ ? 0 : zsl[4] + 1;
-      if (zsl[5] == 0) zph ^= 1;
-      if (jj == 2) pslk = (int)(p0 % G::RP);            // plane k of iteration 3 = P index 0
-      else if (jj > 2) pslk = pslk + 1 == G::RP ? 0 : pslk + 1;
+      for (int q = 0; q < NZW; ++q) zsl[q] = zsl[q + 1];
+      zsl[NZW] = zsl[NZW - 1] + 1 == G::RZ ? 0 : zsl[NZW - 1] + 1;
+      if (zsl[NZW] == 0) zph ^= 1;
+      if (jj == LAG - 1) pslk = (int)(p0 % G::RP);      // plane k of iteration LAG = P index 0
+      else if (jj > LAG - 1) pslk = pslk + 1 == G::RP ? 0 : pslk + 1;
       psl = psl + 1 == G::RP ? 0 : psl + 1;
       if (psl == 0) pph ^= 1;
     }
-    // input planes ke .. ke+3 and (A) P planes ke, ke+1 were only read
+    // input planes ke .. ke+2W-1 and (A) P planes ke .. ke+W-1 were only read
     __syncwarp();
     if (lane == 0) {
       if (!B)
-        for (int q = 0; q < 2; ++q) mbar_arrive(pempty + (p0 + nk + 2 + q) % G::RP);
-      for (int q = 0; q < 4; ++q) mbar_arrive(zempty + (z0 + nk + 4 + q) % G::RZ);
+        for (int q = 0; q < W; ++q) mbar_arrive(pempty + (p0 + nk + W + q) % G::RP);
+      for (int q = 0; q < 2 * W; ++q) mbar_arrive(zempty + (z0 + nk + 2 * W + q) % G::RZ);
     }
-    nz = z0 + nk + 8;
-    np = p0 + nk + 4;
+    nz = z0 + nk + 4 * W;
+    np = p0 + nk + 2 * W;
     // NEXT-3 fused energy monitor (Fig. 1 "Energy"): one partial per item
     // (tile x z-chunk), a fixed shuffle tree then warps in order, so the per-step energy does
     // not depend on which CTA ran the item
@@ -547,22 +569,24 @@ WaveK make_k(const StageLaunch& a) {
   return K;
 }
 
-template <bool B, bool MON>
+template <int W, bool B, bool MON>
 cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
-  using G = Geo<B>;
+  using G = Geo<W, B>;
+  using Q = PG<W>;
   const int nk = a.k_end - a.k_begin;
   if (nk <= 0) return cudaSuccess;
   const Layout& L = a.L;
   const double* in = B ? a.s.c : a.s.y;
   FMaps M;
-  bool ok = enc(&M.rho, in, L, BR_X, BR_Y, 1) && enc(&M.v3, in, L, B3_X, B3_Y, 1) &&
-            enc(&M.v1, in, L, B1_X, B1_Y, 1) && enc(&M.v2, in, L, B2_X, B2_Y, 1) &&
-            enc(&M.yr, a.s.y, L, IR_X, IR_Y, 1) && enc(&M.y1, a.s.y, L, I1_X, I1_Y, 1) &&
-            enc(&M.y2, a.s.y, L, I2_X, I2_Y, 1) && enc(&M.y3, a.s.y, L, I3_X, I3_Y, 1) &&
+  bool ok = enc(&M.rho, in, L, Q::BR_X, Q::BR_Y, 1) && enc(&M.v3, in, L, Q::B3_X, Q::B3_Y, 1) &&
+            enc(&M.v1, in, L, Q::B1_X, Q::B1_Y, 1) && enc(&M.v2, in, L, Q::B2_X, Q::B2_Y, 1) &&
+            enc(&M.yr, a.s.y, L, Q::IR_X, Q::IR_Y, 1) && enc(&M.y1, a.s.y, L, Q::I1_X, Q::I1_Y, 1) &&
+            enc(&M.y2, a.s.y, L, Q::I2_X, Q::I2_Y, 1) && enc(&M.y3, a.s.y, L, Q::I3_X, Q::I3_Y, 1) &&
             enc(&M.q5, a.s.q, L, TX, TY, 5) && enc(&M.yu, a.s.y, L, TX, TY, 1);
   if (!ok) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> attr_done{0};
-  if (cudaError_t e = smem_optin((const void*)wave_fused3<B, MON>, G::SMEM, attr_done); e != cudaSuccess) return e;
+  if (cudaError_t e = smem_optin((const void*)wave_fused3<W, B, MON>, G::SMEM, attr_done); e != cudaSuccess)
+    return e;
   const int nsm = device_sm_count();
   const int ntx = (int)((L.nx + TX - 1) / TX), nty = (int)((L.ny + TY - 1) / TY);
   // z planes per item (128: measured best of 32..512 at 512^3): longer chunks recompute
@@ -578,16 +602,22 @@ cudaError_t launch(const StageLaunch& a, cudaStream_t st) {
   const int nitems = ntx * nty * nchunks;
   const int grid = nitems < nsm ? nitems : nsm;
   const WaveK K = make_k(a);
-  wave_fused3<B, MON><<<grid, NT, G::SMEM, st>>>(M, a, K, chunk, ntx, nty, nitems);
+  wave_fused3<W, B, MON><<<grid, NT, G::SMEM, st>>>(M, a, K, chunk, ntx, nty, nitems);
   return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t pair_w(const StageLaunch& a, int pair, cudaStream_t st) {
+  return pair == 0 ? launch<W, false, false>(a, st)
+                   : (a.mon_partials ? launch<W, true, true>(a, st) : launch<W, true, false>(a, st));
 }
 
 }  // namespace
 
 cudaError_t wave_fused3_pair(const StageLaunch& a, int pair, cudaStream_t st) {
-  if (a.fd_order != 4) return cudaErrorInvalidValue;
-  return pair == 0 ? launch<false, false>(a, st)
-                   : (a.mon_partials ? launch<true, true>(a, st) : launch<true, false>(a, st));
+  if (a.fd_order == 4) return pair_w<2>(a, pair, st);
+  if (a.fd_order == 2) return pair_w<1>(a, pair, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace chemora
