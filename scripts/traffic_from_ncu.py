@@ -36,7 +36,10 @@ def dram(m):
 def wave(path):
     acc = defaultdict(list)
     for _, name, m in launches(path):
-        mm = re.search(r"wave_fused3<(?:\(bool\))?(\d)", name)
+        # template arguments: <W, B, MON> (round-2 final), <B, MON> or <B> (earlier lists)
+        ta = re.search(r"wave_fused3<([^>]*)>", name)
+        args = [re.sub(r"\(\w+\)", "", x).strip() for x in ta.group(1).split(",")] if ta else []
+        mm = re.match(r"(\d)", args[1] if len(args) == 3 else args[0]) if args else None
         if mm:
             acc["wave_fused3<%s>" % "AB"[int(mm.group(1))]].append(dram(m))
     return {k: sum(v[-2:]) / len(v[-2:]) for k, v in acc.items()}
