@@ -280,9 +280,14 @@ int phase_wait(chemora_grid_t g, cudaStream_t st) {
   struct Pop { ~Pop() { nvtxRangePop(); } } pop;
   if (int rc = load_stream_memops()) return rc;
   const uint64_t want = g->epoch;  // neighbours completed phase `epoch`
+  // where the device supports it, the wait also flushes outstanding remote (NVLink peer)
+  // writes, so the neighbours' ghost-plane stores that preceded their flag write are visible
+  // to the kernels after the wait (their flag write already carries a memory barrier)
+  int can_flush = 0;
+  cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, g->desc.device);
+  const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
   for (int f = 0; f < 2; ++f) {
-    CUresult r = g_wait64((CUstream)st, (CUdeviceptr)(g->flags + f), want,
-                          CU_STREAM_WAIT_VALUE_GEQ);
+    CUresult r = g_wait64((CUstream)st, (CUdeviceptr)(g->flags + f), want, flags);
     if (r != CUDA_SUCCESS) return fail(CHEMORA_E_PEER, "cuStreamWaitValue64 failed");
   }
   return CHEMORA_OK;
