@@ -307,15 +307,14 @@ int chemora_read_launch_timing(chemora_grid_t grid, double* ms_sum, int32_t* cou
  * 1 = same in plain order, 2 = register z-march, 3/4 = TMA z-marches (4: every order; the
  * default for orders 6/8 when the 32x16 tiles fill the SMs), 5 = SMEM brick (one kernel per
  * RK stage), 8 = temporally blocked stage pairs on 32x8 tiles with register-queue z stencils
- * (the default for orders 2 and 4, which are the orders it takes); every wave design is
- * bitwise identical.  BSSN: 0 =
+ * (orders 2, 4 and 6: the default there); every wave design is bitwise identical.  BSSN: 0 =
  * two-phase SMEM table, 2 = fissioned G1/G2/G3, 3 = HBM derivative table + algebra kernels,
  * 4 = one fused kernel per stage with the derivatives on chip (SMEM plane tiles by TMA, TMEM
  * z-windows; default); results agree to rounding.  Refused after chemora_grid_connect_ipc. */
 int chemora_set_kernel_variant(chemora_grid_t grid, int variant);
 
 /* The kernel design chemora_rk4_step will run for this handle (the temporally blocked
- * variant 8 falls back to 0 where it does not apply: fd_order 6 or 8). */
+ * variant 8 falls back to 0 where it does not apply: fd_order 8). */
 int chemora_get_kernel_variant(chemora_grid_t grid, int* variant);
 
 /* Copy state set `set` (0 = y, 1 = Q, 2 = B, 3 = C, in the current rotation) padded to host

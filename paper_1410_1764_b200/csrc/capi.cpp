@@ -101,12 +101,12 @@ int radius_of(const chemora_grid_desc& d) {
   return 3;  // BSSN: lopsided upwind stencils reach 3 points
 }
 
-// storage ghost width: the temporally blocked wave kernels (wave_fused3.cu, orders 2 and 4)
+// storage ghost width: the temporally blocked wave kernels (wave_fused3.cu, orders 2, 4, 6)
 // read their inputs with a halo of two stacked radius-W stencils, so those grids keep at least
 // 2W ghost layers in HBM; the API's ghost width (desc.ghost) is unchanged.
 int storage_ghost(const chemora_grid_desc& d) {
   const int order = d.fd_order == 0 ? 4 : d.fd_order;
-  if (d.system == CHEMORA_SYS_WAVE && (order == 2 || order == 4)) return std::max(d.ghost, order);
+  if (d.system == CHEMORA_SYS_WAVE && order <= 6) return std::max(d.ghost, order);
   return d.ghost;
 }
 
@@ -412,8 +412,7 @@ constexpr int kVariantFused3 = 8;
 bool is_fused_variant(int v) { return v == kVariantFused3; }
 bool use_fused(chemora_grid_t g) {
   const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
-  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && (order == 2 || order == 4) &&
-         g->L.g >= order;
+  return g->desc.system == CHEMORA_SYS_WAVE && is_fused_variant(g->variant) && order <= 6 && g->L.g >= order;
 }
 cudaError_t fused_pair(int variant, const StageLaunch& a, int pair, cudaStream_t st) {
   (void)variant;
@@ -539,17 +538,18 @@ int chemora_grid_create(const chemora_grid_desc* desc, void* ws, size_t bytes, c
   g->ipc = false;
   g->cur = 0;
   // default tiling: the temporally blocked stage pairs with register-queue z stencils for
-  // wave grids of order 2 and 4 (variant 8, fastest measured: order 4 profiles/r1_wave_design_study.md,
-  // order 2 7.2 vs 10.5 ms/step at 512^3, profiles/r2_fd_orders.jsonl); orders 6/8: the
-  // persistent TMA z-march when its 32x16 tiles fill the SMs (variant 4: 12.3 vs 15.6-18.1
-  // ms/step at 512^3), else one thread per point; BSSN: the fused per-stage kernel with the
+  // wave grids of order 2, 4 and 6 (variant 8, fastest measured: order 4
+  // profiles/r1_wave_design_study.md; at 512^3 order 2 7.1 vs 10.4, order 6 11.3 vs 12.4 ms/step,
+  // profiles/r2_fd_orders.jsonl); order 8 (radius 4: the pair kernel's rings do not fit shared
+  // memory): the persistent TMA z-march when its 32x16 tiles fill the SMs, else one thread per
+  // point; BSSN: the fused per-stage kernel with the
   // derivatives on chip (variant 4: faster than the HBM-table fission, variant 3, at 192^3
   // with a fifth of its DRAM traffic, profiles/r2_bssn_summary.md)
   {
     const int order = desc->fd_order == 0 ? 4 : desc->fd_order;
     const int64_t tiles16 = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     g->variant = desc->system == CHEMORA_SYS_BSSN ? 4 /* fused, SMEM tiles + TMEM z-windows */
-               : (order == 2 || order == 4) ? kVariantFused3 : (order >= 6 && tiles16 >= 148) ? 4 : 0;
+               : order <= 6 ? kVariantFused3 : tiles16 >= 148 ? 4 : 0;
   }
   // plain 3-D CTA order by default: the banded order cuts DRAM reads by ~10 % but measured
   // slower under the power cap (profiles/r1_wave_summary.md); autotune may pick it (-1)
@@ -851,7 +851,7 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
     const int order = g->desc.fd_order == 0 ? 4 : g->desc.fd_order;
     const int64_t tiles = ((g->L.nx + 31) / 32) * ((g->L.ny + 15) / 16);
     if (tiles >= 148) cands.push_back({4, 0});
-    if ((order == 2 || order == 4) && g->L.g >= order) {
+    if (order <= 6 && g->L.g >= order) {
       cands.push_back({kVariantFused3, 0});
     } else {
       cands.push_back({0, -1});

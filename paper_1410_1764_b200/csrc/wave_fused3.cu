@@ -64,10 +64,13 @@ template <int W> struct PG {
   // iteration t-2, and reads the slot written in t-LAG.  So the warps need not meet at a CTA
   // barrier every plane: each arrives on a per-iteration mbarrier when done and, before
   // writing, waits only until every warp has finished iteration t-2 (the warps may drift one
-  // plane apart).
+  // plane apart; radius 3: t-1).
   static constexpr int LAG = W + 1;
-  static constexpr int RI = LAG + 2;
-  static_assert(NHR <= 32 * NCW - 64 && NH1 <= 32 * NCW && W >= 1, "halo map");
+  // (radius 3: LAG+1 slots -- shared memory is full -- so the warps wait for iteration t-1)
+  static constexpr int RI = W <= 2 ? LAG + 2 : LAG + 1;
+  static constexpr int DW = RI - LAG;             // before writing in iteration t: wait for t-DW
+  static constexpr int NHRT = (NHR + 32 * NCW - 64 - 1) / (32 * NCW - 64);  // IR halo elements per thread
+  static_assert(NH1 <= 32 * NCW && W >= 1 && W <= 3, "halo map");
 };
 // items (tile x z-chunk) are handed out dynamically (an atomic counter, in order), so the
 // items in flight at any time are neighbours in (x, y): their shared halo rows are read by
@@ -79,10 +82,10 @@ template <int W> struct PG {
 template <int W, bool B> struct Geo {
   using Q = PG<W>;
   // input ring depths: resident windows are Z: planes p-LAG .. p+W, P: p-LAG .. p (A) or p
-  // (B), Q: k (B); the rest is prefetch
-  static constexpr int RZ = B ? 8 : 10;
-  static constexpr int RP = B ? 3 : 8;
-  static constexpr int RQ = B ? 3 : 1;  // (A: one unused slot pair keeps the ring arithmetic defined)
+  // (B), Q: k (B); the rest is prefetch (radius 3: one plane each, to fit 227 KB)
+  static constexpr int RZ = W <= 2 ? (B ? 8 : 10) : 2 * W + 3;
+  static constexpr int RP = W <= 2 ? (B ? 3 : 8) : (B ? 2 : W + 3);
+  static constexpr int RQ = B ? (W <= 2 ? 3 : 2) : 1;  // (A: one unused slot pair keeps the ring arithmetic defined)
   static constexpr int PSLOT = Q::P1_B + Q::P2_B + (B ? Q::PY_R + Q::PY_1 + Q::PY_2 + Q::PY_3 : 0);
   static constexpr uint32_t PBYTES =
       (Q::B1_X * Q::B1_Y + Q::B2_X * Q::B2_Y +
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(NT, 1)
     wave_fused3(const __grid_constant__ FMaps M, StageLaunch a, WaveK K, int kchunk, int ntx, int nty, int nitems) {
   using G = Geo<W, B>;
   using Q = PG<W>;
-  constexpr int H = Q::H, WX = Q::WX, LAG = Q::LAG;
+  constexpr int LAG = Q::LAG;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   uint64_t* zfull = bars;
@@ -226,7 +229,6 @@ __global__ void __launch_bounds__(NT, 1)
   // --------------------------------------------------------------------------- consumers
   const int tid = threadIdx.x;
   const int64_t gfs = L.gfs;
-  constexpr int NTC = 32 * NCW;
   const int ti = lane, tj = warp;  // this thread's output point of the tile
   // offset of logical point (x, y) (relative to the tile) in a box of width sx, origin (ox, oy)
   auto at = [](int x, int y, int sx, int ox, int oy) { return (y - oy) * sx + (x - ox); };
@@ -238,18 +240,21 @@ __global__ void __launch_bounds__(NT, 1)
   const int cc = tj * TX + ti;
   // halo elements (logical radius W): the IR ring (threads 64 ..), the I1 side columns
   // (threads 0 ..), the I2 top / bottom rows (threads 0..63, NH2T each)
-  const bool hR = tid >= 64 && tid < 64 + Q::NHR;
-  int hR_c1 = 0, hR_c2 = 0, hR_c3 = 0, hR_b = 0, hR_e = 0;
-  {
+  int hR_c1[Q::NHRT], hR_c2[Q::NHRT], hR_c3[Q::NHRT], hR_b[Q::NHRT], hR_e[Q::NHRT];
+  bool hR[Q::NHRT];
+#pragma unroll
+  for (int u = 0; u < Q::NHRT; ++u) {
     constexpr int RX = TX + 2 * W;  // logical IR row length
-    const int h = hR ? tid - 64 : 0;
+    const int hh = tid - 64 + (32 * NCW - 64) * u;
+    hR[u] = tid >= 64 && hh < Q::NHR;
+    const int h = hR[u] ? hh : 0;
     int x, y;
     if (h < W * RX) { y = -W + h / RX; x = -W + h % RX; }
     else if (h < 2 * W * RX) { y = TY + (h - W * RX) / RX; x = -W + (h - W * RX) % RX; }
     else { const int q = h - 2 * W * RX, c = q % (2 * W); y = q / (2 * W); x = c < W ? -W + c : TX + c - W; }
-    hR_c1 = at(x, y, Q::B1_X, Q::B1_OX, Q::B1_OY); hR_c2 = at(x, y, Q::B2_X, Q::B2_OX, Q::B2_OY);
-    hR_c3 = at(x, y, Q::B3_X, Q::B3_OX, Q::B3_OY); hR_b = at(x, y, Q::BR_X, Q::BR_OX, Q::BR_OY);
-    hR_e = at(x, y, Q::IR_X, Q::IR_OX, Q::IR_OY);
+    hR_c1[u] = at(x, y, Q::B1_X, Q::B1_OX, Q::B1_OY); hR_c2[u] = at(x, y, Q::B2_X, Q::B2_OX, Q::B2_OY);
+    hR_c3[u] = at(x, y, Q::B3_X, Q::B3_OX, Q::B3_OY); hR_b[u] = at(x, y, Q::BR_X, Q::BR_OX, Q::BR_OY);
+    hR_e[u] = at(x, y, Q::IR_X, Q::IR_OX, Q::IR_OY);
   }
   const bool h1 = tid < Q::NH1;
   int h1_cr, h1_b, h1_e;
@@ -324,9 +329,9 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int q = 0; q < LAG; ++q) ips[q] = ips[q + 1];
       ips[LAG] = wslot;
-      // every warp has finished iteration t-2: the slot written now was last read there, and
-      // the slot read now (written in t-3) is complete
-      if (t >= 2) mbar_wait(done + (t - 2) % ND, ((t - 2) / ND) & 1);
+      // every warp has finished iteration t-DW: the slot written now was last read there, and
+      // the slot read now (written in t-LAG) is complete
+      if (t >= Q::DW) mbar_wait(done + (t - Q::DW) % ND, ((t - Q::DW) / ND) & 1);
       double IRown = 0.0, I3own = 0.0;
       if (first) {
         mbar_wait(zfull + zsl[NZW], zph);
@@ -357,17 +362,19 @@ __global__ void __launch_bounds__(NT, 1)
           IRown = fma(cdt, kr, base);
           IR[e_R] = IRown;
         }
-        if (hR) {  // rho at the halo element
-          const double dv1 = d1s_<W>(s1, hR_c1, 1) * K.ih[0];
-          const double dv2 = d1s_<W>(s2, hR_c2, Q::B2_X) * K.ih[1];
-          double dv3 = 0.0;
 #pragma unroll
-          for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[W + q][hR_c3] - z3[W - q][hR_c3], dv3);
-          dv3 = dv3 * K.ih[2];
-          const double kr = dv1 + dv2 + dv3;
-          const double base = B ? sy[hR_e] : zR[W][hR_b];
-          IR[hR_e] = fma(cdt, kr, base);
-        }
+        for (int u = 0; u < Q::NHRT; ++u)
+          if (hR[u]) {  // rho at the halo element(s)
+            const double dv1 = d1s_<W>(s1, hR_c1[u], 1) * K.ih[0];
+            const double dv2 = d1s_<W>(s2, hR_c2[u], Q::B2_X) * K.ih[1];
+            double dv3 = 0.0;
+#pragma unroll
+            for (int q = W; q >= 1; --q) dv3 = fma(D1W<W>::c(q), z3[W + q][hR_c3[u]] - z3[W - q][hR_c3[u]], dv3);
+            dv3 = dv3 * K.ih[2];
+            const double kr = dv1 + dv2 + dv3;
+            const double base = B ? sy[hR_e[u]] : zR[W][hR_b[u]];
+            IR[hR_e[u]] = fma(cdt, kr, base);
+          }
         {  // v1, v2 at the own point
           const double k1v = d1s_<W>(zR[W], o_r, 1) * K.ih[0];
           I1[e_1] = fma(cdt, k1v, B ? sy[PYR + e_1] : s1[o_1]);
@@ -617,6 +624,7 @@ cudaError_t pair_w(const StageLaunch& a, int pair, cudaStream_t st) {
 cudaError_t wave_fused3_pair(const StageLaunch& a, int pair, cudaStream_t st) {
   if (a.fd_order == 4) return pair_w<2>(a, pair, st);
   if (a.fd_order == 2) return pair_w<1>(a, pair, st);
+  if (a.fd_order == 6) return pair_w<3>(a, pair, st);
   return cudaErrorInvalidValue;
 }
 

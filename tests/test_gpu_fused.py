@@ -58,6 +58,17 @@ def test_fused_order2_bitwise_equal_to_stagewise(n, ghost):
     assert np.array_equal(a.get_state(padded=True), b.get_state(padded=True))
 
 
+@pytest.mark.parametrize("n", [(70, 45, 33), (33, 17, 40), (12, 12, 12), (40, 37, 20)])
+def test_fused_order6_bitwise_equal_to_stagewise(n):
+    """The stage pairs at stencil radius 3 (FD order 6): storage ghost 6, the shallowest
+    rings that fit shared memory, warps synchronised per iteration."""
+    a, _ = _run(n, 0, 3, ghost=3, order=6)
+    b, _ = _run(n, 8, 3, ghost=3, order=6)
+    assert b.kernel_variant() == 8
+    assert np.array_equal(a.get_state(), b.get_state())
+    assert np.array_equal(a.get_state(padded=True), b.get_state(padded=True))
+
+
 @pytest.mark.parametrize("fv", FUSED_VARIANTS)
 def test_fused_parity_10_steps(fv):
     n = (48, 40, 56)

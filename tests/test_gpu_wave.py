@@ -196,7 +196,7 @@ def test_wide_stencil_tilings_bitwise_identical(order):
     y0 = ci.noise(n, 5, seed=order)
     dt = 0.2 * min(h)
     out = []
-    variants = (0, 1, 2, 4) + ((8,) if order == 2 else ())  # 8: the order-2 stage pairs
+    variants = (0, 1, 2, 4) + ((8,) if order <= 6 else ())  # 8: the stage pairs (radius 1, 3)
     for v in variants:
         g = P.Grid(C.SYS_WAVE, n, h, ghost=gh, fd_order=order)
         g.set_kernel_variant(v)
@@ -205,7 +205,7 @@ def test_wide_stencil_tilings_bitwise_identical(order):
         out.append(g.get_state())
     for v, o in zip(variants[1:], out[1:]):
         assert np.array_equal(out[0], o), f"order {order}: variant {v} differs"
-    for sv in (4,) + ((8,) if order == 2 else ()):
+    for sv in (4,) + ((8,) if order <= 6 else ()):
         s = P.LocalSlabs(C.SYS_WAVE, n, h, 2, ghost=gh, fd_order=order)
         for gg in s.grids:
             gg.set_kernel_variant(sv)
@@ -268,7 +268,7 @@ def test_fd_order_parity(order):
     dt = 0.2 * min(h)
     y0 = ci.noise(n, 5, seed=order)
     ref = oracle.rk4(W, y0, h, dt, 10, g=4, order=order)
-    for v in (0, 4) + ((8,) if order in (2, 4) else ()):
+    for v in (0, 4) + ((8,) if order <= 6 else ()):
         g = P.Grid(C.SYS_WAVE, n, h, ghost=4, fd_order=order)
         g.set_kernel_variant(v)
         g.set_initial(C.INIT_HOST, y0)
