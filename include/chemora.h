@@ -16,7 +16,10 @@
  *    it to chemora_grid_create(); it must outlive the handle and be 256-byte aligned.
  *  - Streams are borrowed (cudaStream_t passed as void*; NULL = legacy default stream).
  *    Calls ENQUEUE work on the stream and return; device faults and non-finite values
- *    surface at the next synchronising call (chemora_get_state*, chemora_norms*).
+ *    surface at the next synchronising call (chemora_get_state*, chemora_norms*).  The
+ *    calls on one handle must be ordered (one stream, or streams ordered by events): the
+ *    handle's workspace holds its state sets, flags and the kernels' work-item counter.
+ *    Different handles may run concurrently on different streams.
  *  - Every function returns a chemora_status; on failure a thread-local message is
  *    available from chemora_last_error().  No function aborts the process.
  *  - Boundary: periodic on all axes (reading R9).  With nranks > 1
