@@ -1,15 +1,16 @@
-// wave_fused3.cu -- kernel variant 8: the temporally blocked RK4 stage pairs of
-// the round-1 pair kernel (Eq. 1) with the z stencils of each thread's
-// own column taken from register queues (2.5-D z-march inside the temporal blocking).
+// wave_fused3.cu -- kernel variant 8: the temporally blocked RK4 stage pairs (Eq. 1,
+// PAPER.md:320-327) -- stages 1+2 in kernel A, 3+4 in kernel B -- for stencil
+// radius W = 1, 2, 3 (FD orders 2, 4, 6), with the z stencils of each
+// thread's own column taken from register queues (2.5-D z-march inside the temporal blocking).
 //
 // Every consumer thread owns one output point (ti, tj) of the 32x8 tile, and with it the
-// intermediate values at that point (rho, v1, v2, v3); the 176 / 32 / 128 halo elements of
-// the intermediate rho / v1 / v2 planes are spread over the other threads.  The thread keeps
-// its own intermediate rho and v3 for planes p-5 .. p-1 in registers, so the second stage's
-// z stencils and centres need no shared loads and the intermediate v3 never goes to shared
-// memory.  (Keeping the input rho/v3 column in registers too exceeds the 168-register cap
-// of the 9-warp CTA: measured slower.)  Same arithmetic in the
-// same order as the one-kernel-per-stage path (bit-identical; no FMA contraction).
+// intermediate values at that point (rho, v1, v2, v3); the halo elements of the intermediate
+// rho / v1 / v2 planes (176 / 32 / 128 at W = 2) are spread over the other threads.  The thread
+// keeps its own intermediate rho and v3 for planes p-2W-1 .. p-1 in registers, so the second
+// stage's z stencils and centres need no shared loads and the intermediate v3 never goes to
+// shared memory.  (Keeping the input rho/v3 column in registers too exceeds the 168-register
+// cap of the 9-warp CTA: measured slower.)  Same arithmetic in the same order as the
+// one-kernel-per-stage path (bit-identical; no FMA contraction).
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
