@@ -60,6 +60,32 @@ def test_fused_energy_monitor_matches_oracle(n, variant):
     assert np.array_equal(g.read_monitor(), e)
 
 
+@pytest.mark.parametrize("order", [2, 6])
+def test_fused_energy_monitor_other_orders(order):
+    """The monitor instantiation of the stage-pair kernel B at stencil radius 1 and 3: the
+    energy after every step equals the oracle's energy of the oracle's state at that order,
+    and the state is bitwise the unmonitored one."""
+    P, C = _mods()
+    n = (40, 36, 44)
+    h = tuple(2 * math.pi / v for v in n)
+    dt = 0.2 * min(h)
+    y0 = ci.noise(n, 5, seed=30 + order)
+    g = P.Grid(C.SYS_WAVE, n, h, fd_order=order)
+    assert g.kernel_variant() == 8
+    g.set_initial(C.INIT_HOST, y0)
+    g.set_monitor(True)
+    g.rk4_step(dt, 3)
+    e = g.read_monitor()
+    y = y0
+    for s in range(3):
+        y = oracle.rk4(oracle.WAVE, y, h, dt, 1, g=order // 2, order=order)
+        assert e[s] == pytest.approx(oracle.norms(oracle.WAVE, y, h, g=order // 2)[-1], rel=1e-12)
+    ref = P.Grid(C.SYS_WAVE, n, h, fd_order=order)
+    ref.set_initial(C.INIT_HOST, y0)
+    ref.rk4_step(dt, 3)
+    assert np.array_equal(ref.get_state(), g.get_state())
+
+
 def test_dynamic_item_schedule_is_deterministic():
     """The temporally blocked wave kernels hand out their (tile, z-chunk) items dynamically
     (an atomic counter): which CTA runs which item changes from run to run.  On a grid with
