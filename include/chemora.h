@@ -102,7 +102,9 @@ const char* chemora_version(void);
 const char* chemora_last_error(void);
 
 /* Bytes of device workspace the grid needs (4 state sets of n_gf padded arrays: the
- * y/Q/B/C scheme of DESIGN.md §RK4, plus reduction scratch and flags; for BSSN also the
+ * y/Q/B/C scheme of DESIGN.md §RK4, padded with max(ghost, fd_order) layers for wave orders
+ * 2-6 (the stage-pair kernels' halo) and ghost layers otherwise, plus reduction scratch and
+ * flags; for BSSN also the
  * derivative table of kernel variant 3: 136 doubles per local interior point, e.g. 7.7 GB
  * at 192^3).  Validates desc. */
 int chemora_grid_required_bytes(const chemora_grid_desc* desc, size_t* bytes);
