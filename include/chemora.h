@@ -309,10 +309,10 @@ int chemora_read_launch_timing(chemora_grid_t grid, double* ms_sum, int32_t* cou
 /* ---- testing hooks (not part of the user-facing contract) */
 
 /* Select the kernel design of this handle.  WAVE: 0 = one thread per point,
- * 1 = same in plain order, 2 = register z-march, 3/4 = TMA z-marches (4: every order; the
- * default for orders 6/8 when the 32x16 tiles fill the SMs), 5 = SMEM brick (one kernel per
- * RK stage), 8 = temporally blocked stage pairs on 32x8 tiles with register-queue z stencils
- * (orders 2, 4 and 6: the default there); every wave design is bitwise identical.  BSSN: 0 =
+ * 1 = same in plain order, 4 = persistent TMA z-march (every order; the default for order 8
+ * when its 32x16 tiles fill the SMs; one kernel per RK stage), 8 = temporally blocked stage
+ * pairs on 32x8 tiles with register-queue z stencils (orders 2, 4 and 6: the default there);
+ * every wave design is bitwise identical.  BSSN: 0 =
  * two-phase SMEM table, 2 = fissioned G1/G2/G3, 3 = HBM derivative table + algebra kernels,
  * 4 = one fused kernel per stage with the derivatives on chip (SMEM plane tiles by TMA, TMEM
  * z-windows; default); results agree to rounding.  Refused after chemora_grid_connect_ipc. */

@@ -592,7 +592,7 @@ int chemora_get_kernel_variant(chemora_grid_t g, int* variant) {
 
 int chemora_set_kernel_variant(chemora_grid_t g, int variant) {
   if (int rc = check_grid(g)) return rc;
-  const bool ok = g->desc.system == CHEMORA_SYS_WAVE ? (variant >= 0 && variant <= 5) || variant == kVariantFused3
+  const bool ok = g->desc.system == CHEMORA_SYS_WAVE ? (variant == 0 || variant == 1 || variant == 4 || variant == kVariantFused3)
                                                     : (variant == 0 || variant == 2 || variant == 3 || variant == 4);
   if (!ok) return fail(CHEMORA_E_INVALID, "unknown kernel variant " + std::to_string(variant));
   if (g->ipc) return fail(CHEMORA_E_PEER, "the kernel design of a peer-connected slab is fixed at connect time");
@@ -841,9 +841,10 @@ int chemora_autotune(chemora_grid_t g, int32_t trials, int32_t* chosen, double* 
   // candidate tilings (variant, band), pruned by a footprint model:
   //   wave: one thread per point in plain order (L1/L2 reuse of every stencil operand),
   //         the persistent TMA z-march (only when its 32x16 tiles fill the SMs), and for
-  //         4th order the two temporally blocked pair kernels (32x8 tiles: variants 6 and
-  //         8), else the banded L2-window order;
-  //   BSSN: fissioned kernels, and the fused single kernel only for small grids (it spills).
+  //         orders 2-6 the temporally blocked stage pairs (variant 8, when the storage ghost
+  //         holds their halo), else the banded L2-window order;
+  //   BSSN: the fissioned one-thread-per-point kernels, the HBM-table fission and the fused
+  //         per-stage kernel.
   struct Cand { int variant, band; };
   std::vector<Cand> cands;
   if (g->desc.system == CHEMORA_SYS_WAVE) {
