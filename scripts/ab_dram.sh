@@ -1,6 +1,7 @@
 # Same-box A/B of alternative builds with their DRAM traffic: timing (two interleaved rounds,
 # scripts/ab_swap.sh) then one ncu launch list (time + DRAM bytes) per build.
 # usage: bash scripts/ab_dram.sh "<bench args>" A B ...
+mkdir -p ab
 ARGS="$1"; shift
 bash scripts/ab_swap.sh "$ARGS" "$@"
 L=paper_1410_1764_b200/libchemora.so

@@ -3,6 +3,7 @@
 # Usage (on the GPU box):  bash scripts/ab_swap.sh "<bench args>" A B C ...
 #   each name X refers to ab/libX.so (build it here: edit, build, cp the .so to ab/libX.so;
 #   ab/ is git-ignored but travels with the gpurun snapshot).
+mkdir -p ab
 ARGS="$1"; shift
 L=paper_1410_1764_b200/libchemora.so
 cp $L ab/orig.so

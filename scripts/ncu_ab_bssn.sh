@@ -1,4 +1,5 @@
 # ncu --set full of one BSSN fused stage kernel with an alternative build ab/lib$1.so
+mkdir -p ab
 L=paper_1410_1764_b200/libchemora.so
 cp $L ab/orig0.so
 cp ab/lib$1.so $L

@@ -1,4 +1,5 @@
 # A/B of the persistent TMA z-march (wave variant 4, default for FD orders 6/8): tests, timing
+mkdir -p ab
 L=paper_1410_1764_b200/libchemora.so
 cp $L ab/orig0.so
 cp ab/lib$1.so $L

@@ -1,4 +1,5 @@
 # A/B of an alternative wave pair kernel build (ab/lib$1.so): GPU wave tests, then timing
+mkdir -p ab
 L=paper_1410_1764_b200/libchemora.so
 cp $L ab/orig0.so
 cp ab/lib$1.so $L

@@ -1,4 +1,5 @@
 # order-2 pair kernels: tests (wave) + timing of variant 0 vs 8 at order 2, and order 4 A/B vs cur
+mkdir -p ab
 L=paper_1410_1764_b200/libchemora.so
 cp $L ab/orig0.so
 cp ab/lib$1.so $L

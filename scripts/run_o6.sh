@@ -1,4 +1,5 @@
 # order-6 pair kernels (radius 3): tests, timing vs the TMA z-march, order-4 A/B vs cur
+mkdir -p ab
 L=paper_1410_1764_b200/libchemora.so
 cp $L ab/orig0.so
 cp ab/lib$1.so $L
