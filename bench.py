@@ -421,6 +421,20 @@ def main():
                                          "dram_frac_measured its ncu-measured traffic over its live duration")
                 if roofline["traffic"] and config == "wave512":
                     roofline["dram_frac_measured"] = roofline["traffic"] / (avg[dom] * 1e-3) / 1e9 / peak
+                # both stage-pair launches (their durations are close, so which one dominates
+                # varies from run to run)
+                per = {}
+                for s_ in slots:
+                    nm = "wave_fused3<%s>" % "AB"[s_]
+                    e = {"launch_ms_avg": avg[s_],
+                         "frac": WAVE_PAIR_BYTES[s_] * pts_local / (avg[s_] * 1e-3) / 1e9 / peak,
+                         "frac_at_design_bytes": WAVE_PAIR_DESIGN_BYTES[s_] * pts_local / (avg[s_] * 1e-3) / 1e9 / peak}
+                    tr = committed_traffic(config, nm)
+                    if tr and config == "wave512":
+                        e["traffic"] = tr
+                        e["dram_frac_measured"] = tr / (avg[s_] * 1e-3) / 1e9 / peak
+                    per[nm] = e
+                roofline["launches"] = per
         else:
             derived, meas = fp64_peaks()
             flops = BSSN_FLOPS / 4 * pts_local
